@@ -1,0 +1,179 @@
+/*
+ * hlm_b200.h -- C-ABI of the B200-native local-max hypergraph matcher (libhlm_b200.so).
+ *
+ * This is the drop-in boundary for the reference's CPU matching path.  Every entry point names
+ * the reference interface it replaces (file:line relative to /root/reference/proj/include/hlm/).
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.  The C++ shim with
+ * the reference's own signatures is include/hlm_b200.hpp; the Python binding is
+ * paper_2602_22976_b200/_lib.py; the reference-side glue is shown in INTEGRATION.md.
+ *
+ * All entry points return an hlm_b200_status.  On failure hlm_b200_last_error() holds a
+ * message (thread-local).  There is no CPU fallback: without a CUDA device every compute entry
+ * point fails with HLM_B200_ERR_CUDA.
+ */
+#ifndef HLM_B200_H
+#define HLM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HLM_B200_ABI_VERSION 1
+
+typedef enum {
+  HLM_B200_OK = 0,
+  HLM_B200_ERR_INPUT = 1,       /* hlm::input_error   (common.hpp:18)  */
+  HLM_B200_ERR_ROUND_LIMIT = 2, /* hlm::round_limit_error (matching.hpp:77); partial result filled */
+  HLM_B200_ERR_CUDA = 3,        /* CUDA runtime failure / no device */
+  HLM_B200_ERR_NOMEM = 4,
+  HLM_B200_ERR_UNSUPPORTED = 5  /* e.g. a Variant this library does not implement */
+} hlm_b200_status;
+
+/* hlm::GeneratorKind / hlm::WeightMode (weight_stream.hpp:17-22), same enumerator order. */
+enum { HLM_B200_GEN_XORSHIFT = 0, HLM_B200_GEN_PARK_MILLER = 1, HLM_B200_GEN_SPLITMIX = 2 };
+enum { HLM_B200_MODE_PERTURB_BASE = 0, HLM_B200_MODE_REPLACE_UNIFORM = 1 };
+
+/* hlm::Variant (local_max_par.hpp:34), same enumerator order.  Implemented: CRCW, CREW. */
+enum {
+  HLM_B200_VARIANT_SEQ = 0,
+  HLM_B200_VARIANT_CRCW = 1,
+  HLM_B200_VARIANT_CREW = 2,
+  HLM_B200_VARIANT_WORK_OPTIMAL = 3,
+  HLM_B200_VARIANT_GREEDY = 4
+};
+
+/* Borrowed view of hlm::Hypergraph (hypergraph.hpp:19-27): exactly its five arrays.  The vertex
+ * side may be NULL: the library derives the incidence CSR on the device when a variant needs it. */
+typedef struct {
+  uint32_t num_vertices;
+  uint32_t num_edges;
+  const uint64_t* vertex_offsets;   /* n+1, or NULL */
+  const uint32_t* vertex_incidence; /* kappa, or NULL */
+  const uint64_t* edge_offsets;     /* m+1 */
+  const uint32_t* edge_members;     /* kappa = edge_offsets[m] */
+  const double* base_weights;       /* m, all > 0 */
+} hlm_b200_csr_view;
+
+/* hlm::WeightStream (weight_stream.hpp:56-61). */
+typedef struct {
+  uint64_t seed;
+  int32_t kind;
+  int32_t mode;
+  double noise_low;
+  double noise_high;
+} hlm_b200_stream;
+
+enum { HLM_B200_LOOP_AUTO = 0, HLM_B200_LOOP_HOST = 1, HLM_B200_LOOP_GRAPH = 2 };
+enum { HLM_B200_TIES_AUTO = 0, HLM_B200_TIES_EXACT = 1 };
+
+/* hlm::ParallelConfig (local_max_par.hpp:36-42).  workers / grain have no meaning on a GPU and
+ * are absent; assert_exclusive_writes maps to compute-sanitizer runs. */
+typedef struct {
+  int32_t variant;      /* HLM_B200_VARIANT_* */
+  uint32_t max_rounds;  /* 0 selects hlm::default_max_rounds (matching.hpp:87) */
+  int32_t loop_mode;    /* HLM_B200_LOOP_*: host-driven rounds or one CUDA-graph WHILE launch */
+  int32_t tie_mode;     /* HLM_B200_TIES_AUTO: 64-bit keys + detection + exact redo of a tied round;
+                           HLM_B200_TIES_EXACT: three-level (w, tie_hash, id) keys every round */
+  uint32_t flags;       /* HLM_B200_FLAG_* */
+} hlm_b200_config;
+
+#define HLM_B200_FLAG_NO_ROUND_OF 1u /* do not return matched_round */
+
+/* hlm::MatchResult = Matching + RunReport (matching.hpp:15-48), flattened.  Arrays are owned by
+ * the library; release with hlm_b200_result_free.  report.matched_per_round[r] is
+ * { matched_edges[i] : matched_round[i] == r+1 } (already ascending). */
+typedef struct {
+  uint32_t* matched_edges;         /* ascending original ids */
+  uint16_t* matched_round;         /* parallel to matched_edges, 1-based */
+  uint64_t num_matched;
+  double total_weight;             /* sum of base weights in ascending-id order */
+  uint32_t rounds;
+  uint32_t* per_round_matched;     /* rounds entries */
+  uint32_t* per_round_deactivated; /* rounds entries */
+  uint64_t total_edge_visits;      /* WorkCounters by the reference's per-variant formulas */
+  uint64_t total_pin_visits;
+  uint64_t device_edge_visits;     /* what the device really swept: sum over rounds of m_r */
+  uint64_t device_pin_visits;      /* sum over rounds of kappa_r (only counted when cheap; else 0) */
+  double wall_time_ms;             /* host clock around the matching (upload excluded) */
+  double device_ms;                /* CUDA events around the round loop + result assembly */
+  uint32_t tie_redo_rounds;        /* rounds that were redone on the exact three-level path */
+  uint32_t kernel_launches;        /* kernels of this library launched by the call */
+  uint32_t graph_launches;         /* CUDA-graph launches (each runs many rounds) */
+  uint32_t write_conflicts;        /* always 0 (RunReport::write_conflicts) */
+} hlm_b200_result;
+
+typedef struct hlm_b200_graph hlm_b200_graph; /* opaque: instance resident in HBM */
+
+typedef struct {
+  uint32_t num_vertices;
+  uint32_t num_edges;
+  uint64_t num_pins;
+  uint32_t uniform_size;   /* d if every edge has d pins, else 0 */
+  uint32_t max_edge_size;
+  uint32_t num_large_edges; /* edges handled warp-per-edge (size > 32) */
+  int32_t unit_weights;    /* all base weights equal */
+  int32_t device;
+  uint64_t device_bytes;   /* HBM held by the instance + workspace */
+} hlm_b200_graph_info;
+
+/* Synthetic instances generated on the device; the CPU
+ * restatement lives in oracle/hlm_oracle.c (orc_syn_generate) and is checked bit-for-bit. */
+enum { HLM_B200_SYN_UNIFORM = 0, HLM_B200_SYN_RMAT = 1, HLM_B200_SYN_POWERLAW = 2, HLM_B200_SYN_NETLIST = 3 };
+typedef struct {
+  int32_t family;
+  uint32_t n;
+  uint32_t m;
+  uint32_t d;
+  uint32_t scale;
+  uint64_t seed;
+  int32_t int_weights;
+  /* edge-partition for multi-GPU runs: this graph holds edges [edge_begin, edge_begin + m_local)
+   * of the m-edge instance; 0/0 = the whole instance. */
+  uint32_t edge_begin;
+  uint32_t m_local;
+} hlm_b200_syn_spec;
+
+int hlm_b200_abi_version(void);
+const char* hlm_b200_last_error(void);
+int hlm_b200_device_count(void);
+
+/* Loader: replaces the in-memory hand-over of hlm::Hypergraph to run_variant
+ * (tools/hlm_app.hpp:156-165).  Narrows offsets, detects uniform edge size / unit weights, bins
+ * large edges, uploads to HBM.  The host arrays are not retained. */
+int hlm_b200_graph_upload(const hlm_b200_csr_view* host, int device, hlm_b200_graph** out);
+int hlm_b200_graph_generate(const hlm_b200_syn_spec* spec, int device, hlm_b200_graph** out);
+int hlm_b200_graph_info_get(const hlm_b200_graph* g, hlm_b200_graph_info* info);
+/* Copies the instance back into caller-allocated host arrays (any pointer may be NULL);
+ * vertex side is produced by the device incidence builder. */
+int hlm_b200_graph_download(hlm_b200_graph* g, uint64_t* vertex_offsets, uint32_t* vertex_incidence,
+                            uint64_t* edge_offsets, uint32_t* edge_members, double* base_weights);
+void hlm_b200_graph_release(hlm_b200_graph* g);
+
+/* run_variant / local_max_crcw / local_max_crew (local_max_par.hpp:586,190,258) on a resident
+ * instance.  Synchronous and re-entrant per graph handle. */
+int hlm_b200_match(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
+                   hlm_b200_result* out);
+/* Same with host arrays in, result out: upload + match + release (the end-to-end drop-in call). */
+int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* stream,
+                        const hlm_b200_config* cfg, int device, hlm_b200_result* out);
+void hlm_b200_result_free(hlm_b200_result* r);
+
+/* verify_matching (exact.hpp:115-140) on the device. */
+int hlm_b200_verify(hlm_b200_graph* g, const uint32_t* matched, uint64_t count, int* disjoint,
+                    int* maximal, double* weight);
+
+/* WeightStream::weight / tie_hash (weight_stream.hpp:78,86) evaluated by the device code the
+ * kernels use; host arrays in and out.  For bit-exactness tests of the priority keys. */
+int hlm_b200_eval_stream(const hlm_b200_stream* stream, const uint32_t* edges, const uint32_t* rounds,
+                         const double* base, size_t count, double* w_out, uint64_t* t_out, int device);
+
+/* default_max_rounds (matching.hpp:87-89). */
+uint32_t hlm_b200_default_max_rounds(uint32_t num_edges);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HLM_B200_H */

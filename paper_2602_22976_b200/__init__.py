@@ -1,0 +1,28 @@
+"""paper_2602_22976_b200 -- B200-native locally-maximal hypergraph matching (HLM).
+
+Drop-in for the reference's CPU matching path (proj/include/hlm/local_max_par.hpp): hypergraph
+CSR in, matched-edge set and weight out, bit-exact.  The work is done by hand-written sm_100a
+CUDA kernels in lib/libhlm_b200.so (C-ABI: include/hlm_b200.h); this package is the thin host
+mirror of the reference API.  There is no CPU fallback.
+"""
+from ._lib import LIB_PATH, load_library  # noqa: F401
+from .api import (  # noqa: F401
+    DeviceError,
+    DeviceHypergraph,
+    Hypergraph,
+    InputError,
+    MatchResult,
+    Matching,
+    ParallelConfig,
+    RoundLimitError,
+    RunReport,
+    VerificationReport,
+    WeightStream,
+    WorkCounters,
+    default_max_rounds,
+    eval_stream,
+    local_max_crcw,
+    local_max_crew,
+    run_variant,
+    verify_matching,
+)

@@ -1,0 +1,361 @@
+"""Host-side mirror of the reference's matching API (proj/include/hlm/), over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+
+* ``Hypergraph``      -- hypergraph.hpp:19-27 (five arrays, numpy)
+* ``WeightStream``    -- weight_stream.hpp:56-61
+* ``ParallelConfig``  -- local_max_par.hpp:36-42 (``workers`` / ``grain`` accepted and ignored)
+* ``run_variant`` / ``local_max_crcw`` / ``local_max_crew`` -- local_max_par.hpp:586,190,258
+* ``verify_matching`` -- exact.hpp:115-140
+* ``InputError`` / ``RoundLimitError`` -- common.hpp:18, matching.hpp:77-85
+
+All work is done by libhlm_b200.so on the GPU; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+
+GENERATOR_KINDS = {"xorshift": 0, "park_miller": 1, "splitmix": 2}
+WEIGHT_MODES = {"perturb_base": 0, "replace_uniform": 1}
+VARIANTS = {"seq": 0, "crcw": 1, "crew": 2, "work_optimal": 3, "opt": 3, "greedy": 4}
+LOOP_MODES = {"auto": 0, "host": 1, "graph": 2}
+TIE_MODES = {"auto": 0, "exact": 1}
+SYN_FAMILIES = {"uniform": 0, "rmat": 1, "powerlaw": 2, "netlist": 3}
+
+
+class InputError(ValueError):
+    """hlm::input_error (common.hpp:18)."""
+
+
+class RoundLimitError(RuntimeError):
+    """hlm::round_limit_error (matching.hpp:77-85): carries the partial matching and report."""
+
+    def __init__(self, partial: "Matching", report: "RunReport"):
+        super().__init__(f"round limit exceeded with {report.rounds} rounds used")
+        self.partial = partial
+        self.report = report
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no device: the library has no CPU fallback."""
+
+
+@dataclass
+class Hypergraph:
+    num_vertices: int
+    num_edges: int
+    vertex_offsets: Optional[np.ndarray]
+    vertex_incidence: Optional[np.ndarray]
+    edge_offsets: np.ndarray
+    edge_members: np.ndarray
+    base_weights: np.ndarray
+
+    def pin_count(self) -> int:
+        return int(self.edge_members.shape[0])
+
+
+@dataclass
+class WeightStream:
+    seed: int = 1
+    kind: str = "xorshift"
+    mode: str = "perturb_base"
+    noise_low: float = 0.0
+    noise_high: float = 100.0
+
+    def _c(self) -> _lib.Stream:
+        kind = GENERATOR_KINDS[self.kind] if isinstance(self.kind, str) else int(self.kind)
+        mode = WEIGHT_MODES[self.mode] if isinstance(self.mode, str) else int(self.mode)
+        return _lib.Stream(self.seed & 0xFFFFFFFFFFFFFFFF, kind, mode, self.noise_low, self.noise_high)
+
+
+@dataclass
+class ParallelConfig:
+    workers: int = 0          # ignored: the device decides its own parallelism
+    variant: str = "crcw"
+    grain: int = 1024         # ignored
+    max_rounds: int = 0
+    assert_exclusive_writes: bool = False  # see DESIGN.md (compute-sanitizer racecheck)
+    loop_mode: str = "auto"   # B200 extension: "host" | "graph"
+    tie_mode: str = "auto"    # B200 extension: "exact" forces the three-level comparator
+    want_round_of: bool = True
+
+    def _c(self) -> _lib.Config:
+        if isinstance(self.variant, str):
+            if self.variant not in VARIANTS:
+                raise InputError("unknown variant")  # local_max_par.hpp:615
+            variant = VARIANTS[self.variant]
+        else:
+            variant = int(self.variant)
+        return _lib.Config(variant, self.max_rounds, LOOP_MODES[self.loop_mode], TIE_MODES[self.tie_mode],
+                           0 if self.want_round_of else 1)
+
+
+@dataclass
+class Matching:
+    matched_edges: np.ndarray
+    total_weight: float = 0.0
+    rounds_used: int = 0
+    per_round_matched: List[int] = field(default_factory=list)
+
+
+@dataclass
+class WorkCounters:
+    rounds: int = 0
+    total_edge_visits: int = 0
+    total_pin_visits: int = 0
+    prefix_sum_invocations: int = 0
+    compactions: int = 0
+
+
+@dataclass
+class RunReport:
+    rounds: int = 0
+    matched_per_round_count: List[int] = field(default_factory=list)
+    deactivated_per_round: List[int] = field(default_factory=list)
+    matched_round: Optional[np.ndarray] = None   # round of matched_edges[i]; see matched_per_round
+    work: WorkCounters = field(default_factory=WorkCounters)
+    wall_time_ms: float = 0.0
+    write_conflicts: int = 0
+    # B200 extensions
+    device_ms: float = 0.0
+    device_edge_visits: int = 0
+    tie_redo_rounds: int = 0
+    kernel_launches: int = 0
+    graph_launches: int = 0
+    _matched_edges: Optional[np.ndarray] = None
+
+    @property
+    def matched_per_round(self) -> List[np.ndarray]:
+        """RunReport::matched_per_round (matching.hpp:39): ascending ids per round."""
+        if self.matched_round is None:
+            raise ValueError("run with want_round_of=True to get per-round id lists")
+        return [self._matched_edges[self.matched_round == r + 1] for r in range(self.rounds)]
+
+
+@dataclass
+class MatchResult:
+    matching: Matching
+    report: RunReport
+
+
+@dataclass
+class VerificationReport:
+    disjoint: bool
+    maximal: bool
+    weight: float
+
+    def valid(self) -> bool:
+        return self.disjoint and self.maximal
+
+
+def _raise(status: int, what: str):
+    msg = f"{what}: {_lib.last_error()}"
+    if status == _lib.ERR_INPUT:
+        raise InputError(msg)
+    if status == _lib.ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if status == _lib.ERR_NOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def _take(ptr, count, dtype):
+    if count == 0 or not ptr:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(int(count),)).astype(dtype, copy=True)
+
+
+def _convert(status: int, res: _lib.Result) -> MatchResult:
+    lib = _lib.load_library()
+    try:
+        if status not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
+            _raise(status, "hlm_b200_match")
+        matched = _take(res.matched_edges, res.num_matched, np.uint32)
+        round_of = _take(res.matched_round, res.num_matched, np.uint16) if res.matched_round else None
+        prm = _take(res.per_round_matched, res.rounds, np.uint32).tolist()
+        prd = _take(res.per_round_deactivated, res.rounds, np.uint32).tolist()
+        matching = Matching(matched, float(res.total_weight), int(res.rounds), prm)
+        report = RunReport(int(res.rounds), prm, prd, round_of,
+                           WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits)),
+                           float(res.wall_time_ms), int(res.write_conflicts), float(res.device_ms),
+                           int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
+                           int(res.graph_launches), matched)
+    finally:
+        lib.hlm_b200_result_free(C.byref(res))
+    if status == _lib.ERR_ROUND_LIMIT:
+        raise RoundLimitError(matching, report)
+    return MatchResult(matching, report)
+
+
+def _view(h: Hypergraph, keep: list) -> _lib.CsrView:
+    def ptr(a, dtype):
+        if a is None:
+            return None
+        arr = np.ascontiguousarray(a, dtype=dtype)
+        keep.append(arr)
+        return arr.ctypes.data
+
+    return _lib.CsrView(h.num_vertices, h.num_edges, ptr(h.vertex_offsets, np.uint64),
+                        ptr(h.vertex_incidence, np.uint32), ptr(h.edge_offsets, np.uint64),
+                        ptr(h.edge_members, np.uint32), ptr(h.base_weights, np.float64))
+
+
+class DeviceHypergraph:
+    """An instance resident in HBM (the loader's output).  Reusable across matchings, so a bench
+    can time the matching alone with inputs already on the device, as the paper's protocol does
+    (PAPER.md:316-319)."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @classmethod
+    def upload(cls, h: Hypergraph, device: int = 0) -> "DeviceHypergraph":
+        lib = _lib.load_library()
+        keep: list = []
+        view = _view(h, keep)
+        out = C.c_void_p()
+        st = lib.hlm_b200_graph_upload(C.byref(view), device, C.byref(out))
+        if st != _lib.OK:
+            _raise(st, "hlm_b200_graph_upload")
+        return cls(out.value)
+
+    @classmethod
+    def generate(cls, family: str, n: int = 0, m: int = 0, d: int = 0, scale: int = 0, seed: int = 1,
+                 int_weights: bool = False, edge_begin: int = 0, m_local: int = 0,
+                 device: int = 0) -> "DeviceHypergraph":
+        lib = _lib.load_library()
+        spec = _lib.SynSpec(SYN_FAMILIES[family], n, m, d, scale, seed, 1 if int_weights else 0, edge_begin,
+                            m_local)
+        out = C.c_void_p()
+        st = lib.hlm_b200_graph_generate(C.byref(spec), device, C.byref(out))
+        if st != _lib.OK:
+            _raise(st, "hlm_b200_graph_generate")
+        return cls(out.value)
+
+    def info(self) -> _lib.GraphInfo:
+        info = _lib.GraphInfo()
+        _lib.load_library().hlm_b200_graph_info_get(self._h, C.byref(info))
+        return info
+
+    def download(self, with_incidence: bool = False, pinned: bool = False) -> Hypergraph:
+        info = self.info()
+        n, m, k = info.num_vertices, info.num_edges, info.num_pins
+
+        def buf(count, dtype):
+            if pinned:
+                import torch
+
+                t = torch.empty(int(count), dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True)
+                return t.numpy()
+            return np.empty(int(count), dtype=dtype)
+
+        # torch has no uint64/uint32 pinned dtypes in older versions; use same-width ints then view
+        def ubuf(count, dtype):
+            if pinned:
+                signed = {np.dtype(np.uint64): np.int64, np.dtype(np.uint32): np.int32}[np.dtype(dtype)]
+                return buf(count, signed).view(dtype)
+            return np.empty(int(count), dtype=dtype)
+
+        eoff = ubuf(m + 1, np.uint64)
+        pins = ubuf(k, np.uint32)
+        base = buf(m, np.float64)
+        voff = ubuf(n + 1, np.uint64) if with_incidence else None
+        vinc = ubuf(k, np.uint32) if with_incidence else None
+        st = _lib.load_library().hlm_b200_graph_download(
+            self._h, voff.ctypes.data if with_incidence else None, vinc.ctypes.data if with_incidence else None,
+            eoff.ctypes.data, pins.ctypes.data, base.ctypes.data)
+        if st != _lib.OK:
+            _raise(st, "hlm_b200_graph_download")
+        return Hypergraph(n, m, voff, vinc, eoff, pins, base)
+
+    def match(self, stream: WeightStream, cfg: Optional[ParallelConfig] = None) -> MatchResult:
+        cfg = cfg or ParallelConfig()
+        cs, cc = stream._c(), cfg._c()
+        res = _lib.Result()
+        st = _lib.load_library().hlm_b200_match(self._h, C.byref(cs), C.byref(cc), C.byref(res))
+        return _convert(st, res)
+
+    def verify(self, matched_edges) -> VerificationReport:
+        ids = np.ascontiguousarray(matched_edges, dtype=np.uint32)
+        dis, mx, w = C.c_int(0), C.c_int(0), C.c_double(0.0)
+        st = _lib.load_library().hlm_b200_verify(self._h, ids.ctypes.data if ids.size else None, ids.size,
+                                                  C.byref(dis), C.byref(mx), C.byref(w))
+        if st != _lib.OK:
+            _raise(st, "hlm_b200_verify")
+        return VerificationReport(bool(dis.value), bool(mx.value), float(w.value))
+
+    def release(self):
+        if self._h:
+            _lib.load_library().hlm_b200_graph_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.release()
+
+
+def run_variant(h: Hypergraph, stream: WeightStream, cfg: Optional[ParallelConfig] = None,
+                device: int = 0) -> MatchResult:
+    """run_variant (local_max_par.hpp:586): host arrays in, MatchResult out (upload + match)."""
+    cfg = cfg or ParallelConfig()
+    lib = _lib.load_library()
+    keep: list = []
+    view = _view(h, keep)
+    cs, cc = stream._c(), cfg._c()
+    res = _lib.Result()
+    st = lib.hlm_b200_match_host(C.byref(view), C.byref(cs), C.byref(cc), device, C.byref(res))
+    return _convert(st, res)
+
+
+def local_max_crcw(h: Hypergraph, stream: WeightStream, cfg: Optional[ParallelConfig] = None) -> MatchResult:
+    cfg = cfg or ParallelConfig()
+    cfg.variant = "crcw"
+    return run_variant(h, stream, cfg)
+
+
+def local_max_crew(h: Hypergraph, stream: WeightStream, cfg: Optional[ParallelConfig] = None) -> MatchResult:
+    cfg = cfg or ParallelConfig()
+    cfg.variant = "crew"
+    return run_variant(h, stream, cfg)
+
+
+def verify_matching(h: Hypergraph, m: Matching, device: int = 0) -> VerificationReport:
+    """verify_matching (exact.hpp:115-140) on the device."""
+    with DeviceHypergraph.upload(h, device) as g:
+        return g.verify(m.matched_edges)
+
+
+def default_max_rounds(num_edges: int) -> int:
+    return int(_lib.load_library().hlm_b200_default_max_rounds(num_edges))
+
+
+def eval_stream(stream: WeightStream, edges, rounds, base=None, device: int = 0):
+    """WeightStream::weight / tie_hash evaluated by the device code (bit-exactness tests)."""
+    edges = np.ascontiguousarray(edges, dtype=np.uint32)
+    rounds = np.ascontiguousarray(rounds, dtype=np.uint32)
+    w = np.empty(edges.size, dtype=np.float64)
+    t = np.empty(edges.size, dtype=np.uint64)
+    b = None
+    if base is not None:
+        base = np.ascontiguousarray(base, dtype=np.float64)
+        b = base.ctypes.data
+    cs = stream._c()
+    st = _lib.load_library().hlm_b200_eval_stream(C.byref(cs), edges.ctypes.data, rounds.ctypes.data, b, edges.size,
+                                                   w.ctypes.data, t.ctypes.data, device)
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_eval_stream")
+    return w, t

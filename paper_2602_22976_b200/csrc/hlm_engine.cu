@@ -1,0 +1,998 @@
+// hlm_engine.cu -- host side of libhlm_b200.so: loader, round-loop driver (host loop and
+// CUDA-graph WHILE loop), exact tie path, result assembly, verification, C-ABI.
+// Reference boundary: run_variant / local_max_crcw / local_max_crew
+// (local_max_par.hpp:586,190,258); semantics: local_max_par.hpp:93-183, local_max_seq.hpp:74-90.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/hlm_b200.h"
+#include "hlm_engine.h"
+#include "hlm_kernels.cuh"
+
+namespace hlmb {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+#define CU_CHECK(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return HLM_B200_ERR_CUDA;                                                            \
+    }                                                                                      \
+  } while (0)
+
+#define ST_CHECK(expr)                 \
+  do {                                 \
+    int _s = (expr);                   \
+    if (_s != HLM_B200_OK) return _s;  \
+  } while (0)
+
+static int bitlen64(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+static uint64_t dbits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
+uint32_t default_max_rounds(uint32_t m) {  // matching.hpp:87-89, common.hpp:27-35
+  const uint64_t x = static_cast<uint64_t>(m) + 2;
+  uint32_t r = 0;
+  uint64_t p = 1;
+  while (p < x) {
+    p <<= 1;
+    ++r;
+  }
+  return 64 + 4 * r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// device instance
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+static int dev_alloc(T** p, size_t count, Graph* g) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HLM_B200_ERR_NOMEM : HLM_B200_ERR_CUDA;
+  }
+  if (g) g->device_bytes += count * sizeof(T);
+  return HLM_B200_OK;
+}
+
+static void dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+void Workspace::release() {
+  dev_free(ctrl);
+  dev_free(vkey);
+  dev_free(dead);
+  dev_free(mround);
+  for (int c = 0; c < 2; ++c) {
+    for (int b = 0; b < 2; ++b) dev_free(list[c][b]);
+    dev_free(mflag[c]);
+  }
+  dev_free(matched_cnt);
+  dev_free(deact_cnt);
+  dev_free(va);
+  dev_free(vb);
+  dev_free(vc);
+  dev_free(chunk_cnt);
+  dev_free(scan_total);
+  dev_free(out_ids);
+  dev_free(out_round);
+  dev_free(out_w);
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  if (graph) cudaGraphDestroy(graph);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  *this = Workspace();
+}
+
+Graph::~Graph() {
+  cudaSetDevice(device);
+  ws.release();
+  crew_release(this);
+  dev_free(pins);
+  dev_free(off32);
+  dev_free(off64);
+  dev_free(base);
+  dev_free(large_list);
+  dev_free(voff);
+  dev_free(vinc);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+EdgeCsr Graph::csr() const {
+  EdgeCsr c;
+  c.pins = pins;
+  c.off32 = off32;
+  c.off64 = off64;
+  c.uniform_d = uniform_d;
+  return c;
+}
+
+static int grid_for(const Graph* g, uint64_t items, int per_block = kBlock) {
+  const uint64_t want = (items + per_block - 1) / per_block;
+  const uint64_t cap = static_cast<uint64_t>(g->num_sms) * 8;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+static int init_device(Graph* g, int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    set_error("no CUDA device available (%s); libhlm_b200 has no CPU fallback",
+              e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+    return HLM_B200_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    set_error("device %d out of range [0, %d)", device, count);
+    return HLM_B200_ERR_INPUT;
+  }
+  CU_CHECK(cudaSetDevice(device));
+  g->device = device;
+  CU_CHECK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CU_CHECK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  return HLM_B200_OK;
+}
+
+// Classifies the resident CSR: uniform size, offsets width, large-edge list, weight constants.
+// `off64_dev` (m+1 entries) is consumed: kept, narrowed or dropped.
+int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins) {
+  cudaStream_t s = g->stream;
+  const uint32_t m = g->m;
+  EdgeStats* d_st = nullptr;
+  ST_CHECK(dev_alloc(&d_st, 1, nullptr));
+  EdgeStats st = {0xffffffffu, 0, 0, 0, 0, 0};
+  CU_CHECK(cudaMemcpyAsync(d_st, &st, sizeof(st), cudaMemcpyHostToDevice, s));
+  if (m) {
+    k_edge_size_stats<<<grid_for(g, m), kBlock, 0, s>>>(off64_dev, m, d_st);
+    if (check_pins && g->kappa) k_max_pin<<<grid_for(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, d_st);
+  }
+  CU_CHECK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, s));
+  CU_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_st);
+  if (st.bad_offsets) {
+    cudaFree(off64_dev);
+    set_error("edge_offsets are not monotone");
+    return HLM_B200_ERR_INPUT;
+  }
+  if (m && st.min_size == 0) {
+    cudaFree(off64_dev);
+    set_error("an edge is empty (hypergraph.hpp:91)");
+    return HLM_B200_ERR_INPUT;
+  }
+  if (check_pins && g->kappa && st.max_pin >= g->n) {
+    cudaFree(off64_dev);
+    set_error("vertex id %u out of range [0, %u)", st.max_pin, g->n);
+    return HLM_B200_ERR_INPUT;
+  }
+  g->max_edge_size = st.max_size;
+  g->num_large = st.num_large;
+  if (m && st.min_size == st.max_size) {
+    g->uniform_d = st.max_size;
+    cudaFree(off64_dev);
+  } else if (m == 0) {
+    cudaFree(off64_dev);
+  } else if (g->kappa < (1ull << 32)) {
+    ST_CHECK(dev_alloc(&g->off32, static_cast<size_t>(m) + 1, g));
+    k_narrow_offsets<<<grid_for(g, m + 1ull), kBlock, 0, s>>>(off64_dev, g->off32, m + 1ull);
+    CU_CHECK(cudaStreamSynchronize(s));
+    cudaFree(off64_dev);
+  } else {
+    g->off64 = off64_dev;
+    g->device_bytes += (static_cast<size_t>(m) + 1) * 8;
+  }
+  if (g->num_large) {
+    ST_CHECK(dev_alloc(&g->large_list, g->num_large, g));
+    uint32_t* d_cnt = nullptr;
+    ST_CHECK(dev_alloc(&d_cnt, 1, nullptr));
+    CU_CHECK(cudaMemsetAsync(d_cnt, 0, 4, s));
+    k_collect_large<<<grid_for(g, m), kBlock, 0, s>>>(g->csr(), m, g->large_list, d_cnt);
+    CU_CHECK(cudaStreamSynchronize(s));
+    cudaFree(d_cnt);
+  }
+  CU_CHECK(cudaGetLastError());
+  return HLM_B200_OK;
+}
+
+// Weight constants: min / max of the base weights; drops the array when all are equal.
+int finish_weights(Graph* g) {
+  if (g->m == 0 || !g->base) return HLM_B200_OK;
+  WeightStats ws;
+  ST_CHECK(weight_stats(g, 0.0, &ws));
+  if (ws.non_positive) {
+    set_error("an edge has a non-positive weight (hypergraph.hpp:104)");
+    return HLM_B200_ERR_INPUT;
+  }
+  std::memcpy(&g->base_min, &ws.min_bits, 8);
+  std::memcpy(&g->base_max, &ws.max_bits, 8);
+  if (ws.min_bits == ws.max_bits) {
+    g->base_const = g->base_min;
+    cudaFree(g->base);
+    g->device_bytes -= static_cast<size_t>(g->m) * 8;
+    g->base = nullptr;
+  }
+  return HLM_B200_OK;
+}
+
+int weight_stats(Graph* g, double lo, WeightStats* out) {
+  WeightStats* d = nullptr;
+  ST_CHECK(dev_alloc(&d, 1, nullptr));
+  WeightStats init = {~0ull, 0ull, 0u, 0u};
+  CU_CHECK(cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, g->stream));
+  k_weight_stats<<<grid_for(g, g->m), kBlock, 0, g->stream>>>(g->base, g->m, lo, d);
+  CU_CHECK(cudaMemcpyAsync(out, d, sizeof(*out), cudaMemcpyDeviceToHost, g->stream));
+  CU_CHECK(cudaStreamSynchronize(g->stream));
+  cudaFree(d);
+  return HLM_B200_OK;
+}
+
+int new_graph(int device, Graph** out) {
+  Graph* g = new (std::nothrow) Graph();
+  if (!g) return HLM_B200_ERR_NOMEM;
+  int rc = init_device(g, device);
+  if (rc != HLM_B200_OK) {
+    g->device = device < 0 ? 0 : device;
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return HLM_B200_OK;
+}
+
+static int upload(const hlm_b200_csr_view* h, int device, Graph** out) {
+  *out = nullptr;
+  if (!h || (h->num_edges && (!h->edge_offsets || !h->base_weights))) {
+    set_error("null hypergraph arrays");
+    return HLM_B200_ERR_INPUT;
+  }
+  Graph* g = nullptr;
+  ST_CHECK(new_graph(device, &g));
+  auto fail = [&](int rc) {
+    delete g;
+    return rc;
+  };
+  g->n = h->num_vertices;
+  g->m = h->num_edges;
+  const uint32_t m = g->m;
+  g->kappa = m ? h->edge_offsets[m] : 0;
+  if (m && h->edge_offsets[0] != 0) {
+    set_error("edge_offsets[0] != 0");
+    return fail(HLM_B200_ERR_INPUT);
+  }
+  if (g->kappa && !h->edge_members) {
+    set_error("null edge_members");
+    return fail(HLM_B200_ERR_INPUT);
+  }
+  cudaStream_t s = g->stream;
+  int rc;
+  if ((rc = dev_alloc(&g->pins, g->kappa, g)) != HLM_B200_OK) return fail(rc);
+  uint64_t* off64 = nullptr;
+  if ((rc = dev_alloc(&off64, static_cast<size_t>(m) + 1, nullptr)) != HLM_B200_OK) return fail(rc);
+  if ((rc = dev_alloc(&g->base, m, g)) != HLM_B200_OK) return fail(rc);
+  cudaError_t e = cudaSuccess;
+  if (m) {
+    e = cudaMemcpyAsync(off64, h->edge_offsets, (static_cast<size_t>(m) + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && g->kappa)
+      e = cudaMemcpyAsync(g->pins, h->edge_members, g->kappa * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(g->base, h->base_weights, static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, s);
+  }
+  if (e != cudaSuccess) {
+    set_error("host-to-device copy failed: %s", cudaGetErrorString(e));
+    cudaFree(off64);
+    return fail(HLM_B200_ERR_CUDA);
+  }
+  g->h2d_bytes = (static_cast<uint64_t>(m) + 1) * 8 + g->kappa * 4 + static_cast<uint64_t>(m) * 8;
+  if ((rc = finish_graph(g, off64, true)) != HLM_B200_OK) return fail(rc);
+  if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
+  *out = g;
+  return HLM_B200_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// workspace + key scheme
+// ---------------------------------------------------------------------------------------------
+static int ensure_workspace(Graph* g, uint32_t max_rounds) {
+  Workspace& w = g->ws;
+  if (!w.ctrl) {
+    ST_CHECK(dev_alloc(&w.ctrl, 1, g));
+    ST_CHECK(dev_alloc(&w.vkey, g->n, g));
+    ST_CHECK(dev_alloc(&w.dead, (static_cast<size_t>(g->n) + 31) / 32, g));
+    ST_CHECK(dev_alloc(&w.mround, g->m, g));
+    for (int b = 0; b < 2; ++b) {
+      ST_CHECK(dev_alloc(&w.list[0][b], g->m, g));
+      ST_CHECK(dev_alloc(&w.list[1][b], g->num_large, g));
+    }
+    ST_CHECK(dev_alloc(&w.mflag[0], g->m, g));
+    ST_CHECK(dev_alloc(&w.mflag[1], g->num_large, g));
+    w.num_chunks = (g->m + kAsmChunk - 1) / kAsmChunk;
+    ST_CHECK(dev_alloc(&w.chunk_cnt, w.num_chunks, g));
+    ST_CHECK(dev_alloc(&w.scan_total, 1, g));
+    CU_CHECK(cudaEventCreate(&w.ev0));
+    CU_CHECK(cudaEventCreate(&w.ev1));
+  }
+  if (w.rounds_cap < max_rounds + 3) {
+    dev_free(w.matched_cnt);
+    dev_free(w.deact_cnt);
+    w.rounds_cap = max_rounds + 3;
+    ST_CHECK(dev_alloc(&w.matched_cnt, w.rounds_cap, g));
+    ST_CHECK(dev_alloc(&w.deact_cnt, w.rounds_cap, g));
+    if (w.graph_exec) {  // captured kernel arguments point at the old arrays
+      cudaGraphExecDestroy(w.graph_exec);
+      cudaGraphDestroy(w.graph);
+      w.graph_exec = nullptr;
+      w.graph = nullptr;
+    }
+  }
+  return HLM_B200_OK;
+}
+
+static int ensure_exact_arrays(Graph* g) {
+  Workspace& w = g->ws;
+  if (w.va) return HLM_B200_OK;
+  ST_CHECK(dev_alloc(&w.va, g->n, g));
+  ST_CHECK(dev_alloc(&w.vb, g->n, g));
+  ST_CHECK(dev_alloc(&w.vc, g->n, g));
+  return HLM_B200_OK;
+}
+
+// Picks the 64-bit key layout for this (instance, stream) pair; see hlm_priority.cuh.
+static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_rounds, KeyScheme* ks) {
+  std::memset(ks, 0, sizeof(*ks));
+  double wmin, wmax;
+  bool int_hash = false;
+  uint64_t wq_min = 0, wq_span = 0;
+  if (sp.mode == HLM_B200_MODE_REPLACE_UNIFORM) {
+    wmin = 0x1.0p-54;  // to_unit_interval_64(0) (weight_stream.hpp:49-52); park-miller >= 1/(2^31-1)
+    wmax = 1.0;
+  } else if (sp.width != 0.0) {
+    wmin = g->base_min + sp.lo;
+    wmax = (g->base_max + sp.lo) + sp.width;  // u < 1 and rounding is monotone
+  } else {
+    wmin = g->base_min + sp.lo;
+    wmax = g->base_max + sp.lo;
+    if (!g->base) {
+      int_hash = true;  // every edge has the same weight: order is (tie_hash, id)
+      wq_min = static_cast<uint64_t>(wmin);
+    } else {
+      WeightStats ws;
+      ST_CHECK(weight_stats(g, sp.lo, &ws));
+      if (!ws.non_integer && wmax - wmin < 65536.0) {
+        int_hash = true;
+        wq_min = static_cast<uint64_t>(wmin);
+        wq_span = static_cast<uint64_t>(wmax) - wq_min;
+      }
+    }
+  }
+  if (int_hash) {
+    const int qb = bitlen64(wq_span);
+    int tag_bits = std::max(8, bitlen64(max_rounds));
+    if (tag_bits > 16) tag_bits = 16;
+    ks->kind = KEY_INT_HASH;
+    ks->payload_bits = 64 - tag_bits;
+    ks->hash_bits = ks->payload_bits - qb;
+    ks->wq_min = wq_min;
+    ks->tag_period = (1u << tag_bits) - 1u;
+    return HLM_B200_OK;
+  }
+  const uint64_t span = dbits(wmax) - dbits(wmin);
+  ks->kind = KEY_WEIGHT_BITS;
+  ks->payload_bits = std::max(1, bitlen64(span));
+  ks->wmin_bits = dbits(wmin);
+  const int tag_bits = 64 - ks->payload_bits;
+  ks->tag_period = tag_bits >= 16 ? 65535u : ((1u << tag_bits) - 1u);
+  return HLM_B200_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// round loop
+// ---------------------------------------------------------------------------------------------
+struct Launcher {
+  Graph* g;
+  RoundParams P;
+  bool exact;  // TIES_EXACT: no 64-bit keys at all
+  uint32_t launches = 0;
+
+  template <bool VMAX>
+  void filter(cudaStream_t s) {
+    const int grid = g->round_grid;
+    switch (g->uniform_d) {
+      case 2: k_filter_vmax_small<2, VMAX><<<grid, kBlock, 0, s>>>(P); break;
+      case 4: k_filter_vmax_small<4, VMAX><<<grid, kBlock, 0, s>>>(P); break;
+      case 8: k_filter_vmax_small<8, VMAX><<<grid, kBlock, 0, s>>>(P); break;
+      default: k_filter_vmax_small<0, VMAX><<<grid, kBlock, 0, s>>>(P); break;
+    }
+    ++launches;
+    if (g->num_large) {
+      k_filter_vmax_large<VMAX><<<g->large_grid, kBlock, 0, s>>>(P);
+      ++launches;
+    }
+  }
+  void check(cudaStream_t s) {
+    const int grid = g->round_grid;
+    switch (g->uniform_d) {
+      case 2: k_check_commit_small<2><<<grid, kBlock, 0, s>>>(P); break;
+      case 4: k_check_commit_small<4><<<grid, kBlock, 0, s>>>(P); break;
+      case 8: k_check_commit_small<8><<<grid, kBlock, 0, s>>>(P); break;
+      default: k_check_commit_small<0><<<grid, kBlock, 0, s>>>(P); break;
+    }
+    ++launches;
+    if (g->num_large) {
+      k_check_commit_large<<<g->large_grid, kBlock, 0, s>>>(P);
+      ++launches;
+    }
+  }
+  void advance(cudaStream_t s, cudaGraphConditionalHandle h, int in_graph) {
+    k_advance<<<1, 1, 0, s>>>(P, h, in_graph);
+    ++launches;
+  }
+};
+
+// Exact three-level argmax + commit for round `r` over the lists in buffer `buf`.
+static int exact_round(Launcher& L, uint32_t r, uint32_t buf, const Ctrl& c) {
+  Graph* g = L.g;
+  Workspace& w = g->ws;
+  cudaStream_t s = g->stream;
+  ST_CHECK(ensure_exact_arrays(g));
+  CU_CHECK(cudaMemsetAsync(w.va, 0, static_cast<size_t>(g->n) * 8, s));
+  CU_CHECK(cudaMemsetAsync(w.vb, 0, static_cast<size_t>(g->n) * 8, s));
+  CU_CHECK(cudaMemsetAsync(w.vc, 0, static_cast<size_t>(g->n) * 4, s));
+  ExactParams X[2];
+  for (int cls = 0; cls < 2; ++cls) {
+    X[cls].va = w.va;
+    X[cls].vb = w.vb;
+    X[cls].vc = w.vc;
+    X[cls].list = (cls == 0 && L.P.ident0 && r == 1) ? nullptr : w.list[cls][buf];
+    X[cls].count = c.count[buf][cls];
+    X[cls].round = r;
+    X[cls].cls = cls;
+    X[cls].mflag = w.mflag[cls];
+  }
+  auto level = [&](int lv) {
+    for (int cls = 0; cls < 2; ++cls) {
+      if (X[cls].count == 0) continue;
+      const int grid = grid_for(g, X[cls].count, kWarpsPerBlock);
+      switch (lv) {
+        case 1: k_exact_level<1><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
+        case 2: k_exact_level<2><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
+        case 3: k_exact_level<3><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
+        default: k_exact_level<4><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
+      }
+      ++L.launches;
+    }
+  };
+  for (int lv = 1; lv <= 4; ++lv) level(lv);
+  CU_CHECK(cudaGetLastError());
+  return HLM_B200_OK;
+}
+
+static int build_loop_graph(Launcher& L) {
+  Graph* g = L.g;
+  Workspace& w = g->ws;
+  if (w.graph_exec) {
+    cudaGraphExecDestroy(w.graph_exec);
+    cudaGraphDestroy(w.graph);
+    w.graph_exec = nullptr;
+    w.graph = nullptr;
+  }
+  CU_CHECK(cudaGraphCreate(&w.graph, 0));
+  cudaGraphConditionalHandle handle;
+  CU_CHECK(cudaGraphConditionalHandleCreate(&handle, w.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = handle;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CU_CHECK(cudaGraphAddNode(&node, w.graph, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  CU_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    const uint32_t before = L.launches;
+    L.filter<true>(cs);
+    L.check(cs);
+    L.advance(cs, handle, 1);
+    w.graph_body_launches = L.launches - before;
+    L.launches = before;
+    e = cudaStreamEndCapture(cs, nullptr);
+  }
+  cudaStreamDestroy(cs);
+  if (e != cudaSuccess) {
+    set_error("CUDA graph capture failed: %s", cudaGetErrorString(e));
+    return HLM_B200_ERR_CUDA;
+  }
+  CU_CHECK(cudaGraphInstantiate(&w.graph_exec, w.graph, 0));
+  w.graph_key = L.P;
+  return HLM_B200_OK;
+}
+
+static bool same_params(const RoundParams& a, const RoundParams& b) {
+  return std::memcmp(&a, &b, sizeof(RoundParams)) == 0;
+}
+
+int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);
+int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant, hlm_b200_result* out);
+
+int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+  const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
+  if (max_rounds > 65000u) {
+    set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
+    return HLM_B200_ERR_UNSUPPORTED;
+  }
+  cudaStream_t s = g->stream;
+  ST_CHECK(ensure_workspace(g, max_rounds));
+  Workspace& w = g->ws;
+
+  Launcher L;
+  L.g = g;
+  L.exact = cfg->tie_mode == HLM_B200_TIES_EXACT;
+  RoundParams& P = L.P;
+  std::memset(&P, 0, sizeof(P));
+  P.csr = g->csr();
+  P.base = g->base;
+  P.base_const = g->base_const;
+  P.n = g->n;
+  P.m = g->m;
+  P.has_large = g->num_large ? 1u : 0u;
+  P.id_base = g->id_base;
+  P.stream.seed = st->seed;
+  P.stream.kind = st->kind;
+  P.stream.mode = st->mode;
+  P.stream.lo = st->noise_low;
+  P.stream.hi = st->noise_high;
+  P.stream.width = st->noise_high - st->noise_low;
+  ST_CHECK(choose_key_scheme(g, P.stream, max_rounds, &P.ks));
+  P.ctrl = w.ctrl;
+  P.vkey = w.vkey;
+  P.dead = w.dead;
+  P.mround = w.mround;
+  for (int c = 0; c < 2; ++c) {
+    for (int b = 0; b < 2; ++b) P.list[c][b] = w.list[c][b];
+    P.mflag[c] = w.mflag[c];
+  }
+  P.ident0 = 1;
+  P.matched_cnt = w.matched_cnt;
+  P.deact_cnt = w.deact_cnt;
+
+  if (!g->round_grid) {
+    int occ = 0;
+    CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_vmax_small<4, true>, kBlock, 0));
+    g->round_grid = g->num_sms * std::max(1, occ);
+    g->large_grid = g->num_sms * 4;
+  }
+
+  bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact;
+  if (use_graph && (!w.graph_exec || !same_params(w.graph_key, P))) ST_CHECK(build_loop_graph(L));
+
+  CU_CHECK(cudaEventRecord(w.ev0, s));
+  // per-call state
+  Ctrl c0;
+  std::memset(&c0, 0, sizeof(c0));
+  c0.round = 1;
+  c0.count[0][0] = g->m;
+  c0.count[0][1] = g->num_large;
+  c0.max_rounds = max_rounds;
+  CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+  CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+  CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.mround, 0, static_cast<size_t>(g->m) * 2, s));
+  CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+  if (g->num_large)
+    CU_CHECK(cudaMemcpyAsync(w.list[1][0], g->large_list, static_cast<size_t>(g->num_large) * 4,
+                             cudaMemcpyDeviceToDevice, s));
+
+  Ctrl c = c0;
+  uint32_t tie_redo = 0, graph_launches = 0;
+  if (g->m == 0) {
+    c.status = ST_DONE;
+  } else {
+    for (;;) {
+      if (use_graph) {
+        CU_CHECK(cudaGraphLaunch(w.graph_exec, s));
+        ++graph_launches;
+      } else if (L.exact) {
+        L.filter<false>(s);
+        // the exact levels need the list lengths on the host
+        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_CHECK(cudaStreamSynchronize(s));
+        if (c.round <= max_rounds) ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
+        L.advance(s, 0, 0);
+      } else {
+        L.filter<true>(s);
+        L.check(s);
+        L.advance(s, 0, 0);
+      }
+      CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+      CU_CHECK(cudaStreamSynchronize(s));
+      if (c.status == ST_RUNNING) continue;
+      if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
+      if (c.status == ST_TIE) {
+        // a vertex saw two equal 64-bit keys in round c.round: redo that round exactly
+        ++tie_redo;
+        ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
+        CU_CHECK(cudaMemsetAsync(&w.ctrl->tie_flag, 0, 4, s));
+        L.advance(s, 0, 0);
+        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_CHECK(cudaStreamSynchronize(s));
+        if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
+      }
+      if (c.status == ST_EPOCH) CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+      if (c.status == ST_TIE) {
+        set_error("internal: tie flag survived the exact redo");
+        return HLM_B200_ERR_CUDA;
+      }
+    }
+  }
+  CU_CHECK(cudaGetLastError());
+  const uint32_t rounds = c.rounds_done;
+  out->tie_redo_rounds = tie_redo;
+  out->graph_launches = graph_launches;
+  out->device_edge_visits = c.edges_swept;
+  w.launches = L.launches + graph_launches * w.graph_body_launches * 0;  // refined below
+  // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
+  out->kernel_launches = L.launches + (use_graph ? (rounds + 1) * w.graph_body_launches : 0);
+  int rc = assemble_result(g, rounds, cfg, HLM_B200_VARIANT_CRCW, out);
+  if (rc != HLM_B200_OK) return rc;
+  return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
+}
+
+// finish_matching (local_max_seq.hpp:74-83) + the RunReport counters.
+int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
+                    hlm_b200_result* out) {
+  Workspace& w = g->ws;
+  cudaStream_t s = g->stream;
+  const uint32_t m = g->m;
+  uint64_t total = 0;
+  if (m) {
+    k_assemble_count<<<w.num_chunks, kBlock, 0, s>>>(w.mround, m, w.chunk_cnt);
+    k_scan_small<<<1, 1024, 0, s>>>(w.chunk_cnt, w.num_chunks, w.scan_total);
+    CU_CHECK(cudaMemcpyAsync(&total, w.scan_total, 8, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+    out->kernel_launches += 2;
+  }
+  const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
+  const bool need_w = g->base != nullptr;
+  if (total > w.out_cap) {
+    dev_free(w.out_ids);
+    dev_free(w.out_round);
+    dev_free(w.out_w);
+    w.out_ids = nullptr;
+    w.out_round = nullptr;
+    w.out_w = nullptr;
+    w.out_cap = total + total / 8 + 1024;
+    ST_CHECK(dev_alloc(&w.out_ids, w.out_cap, g));
+    ST_CHECK(dev_alloc(&w.out_round, w.out_cap, g));
+    if (need_w) ST_CHECK(dev_alloc(&w.out_w, w.out_cap, g));
+  }
+  out->num_matched = total;
+  out->rounds = rounds;
+  out->matched_edges = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (total + 1)));
+  out->matched_round = want_round ? static_cast<uint16_t*>(std::malloc(sizeof(uint16_t) * (total + 1))) : nullptr;
+  out->per_round_matched = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
+  out->per_round_deactivated = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
+  if (!out->matched_edges || !out->per_round_matched || !out->per_round_deactivated ||
+      (want_round && !out->matched_round)) {
+    set_error("host allocation of the result failed");
+    return HLM_B200_ERR_NOMEM;
+  }
+  std::vector<double> wts;
+  if (total) {
+    k_assemble_write<<<w.num_chunks, kBlock, 0, s>>>(w.mround, m, w.chunk_cnt, g->base, g->id_base, w.out_ids,
+                                                     want_round ? w.out_round : nullptr,
+                                                     need_w ? w.out_w : nullptr);
+    out->kernel_launches += 1;
+    CU_CHECK(cudaMemcpyAsync(out->matched_edges, w.out_ids, total * 4, cudaMemcpyDeviceToHost, s));
+    if (want_round)
+      CU_CHECK(cudaMemcpyAsync(out->matched_round, w.out_round, total * 2, cudaMemcpyDeviceToHost, s));
+    if (need_w) {
+      wts.resize(total);
+      CU_CHECK(cudaMemcpyAsync(wts.data(), w.out_w, total * 8, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  if (rounds) {
+    CU_CHECK(cudaMemcpyAsync(out->per_round_matched, w.matched_cnt + 1, rounds * 4ull, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaMemcpyAsync(out->per_round_deactivated, w.deact_cnt + 1, rounds * 4ull, cudaMemcpyDeviceToHost, s));
+  }
+  CU_CHECK(cudaEventRecord(w.ev1, s));
+  CU_CHECK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CU_CHECK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+  out->device_ms = ms;
+  // total_weight accumulates base weights in ascending-id order (local_max_seq.hpp:79)
+  double tw = 0.0;
+  if (need_w) {
+    for (uint64_t i = 0; i < total; ++i) tw += wts[i];
+  } else {
+    const double b = g->base_const;
+    if (b == std::floor(b) && b * static_cast<double>(total) < 9007199254740992.0) {
+      tw = b * static_cast<double>(total);  // exact: every partial sum is an integer below 2^53
+    } else {
+      for (uint64_t i = 0; i < total; ++i) tw += b;
+    }
+  }
+  out->total_weight = tw;
+  // WorkCounters by the reference's formulas (local_max_par.hpp:135,159,164,224,248 for crcw;
+  // :135,159,164,285,299,320-321 for crew): soft-deletion variants charge the full structure
+  // every round.
+  const uint64_t per_round_edges = variant == HLM_B200_VARIANT_CREW ? 5ull : 3ull;
+  const uint64_t per_round_pins = variant == HLM_B200_VARIANT_CREW ? 4ull : 3ull;
+  out->total_edge_visits = per_round_edges * m * rounds;
+  out->total_pin_visits = per_round_pins * g->kappa * rounds;
+  out->write_conflicts = 0;
+  return HLM_B200_OK;
+}
+
+int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!g || !st || !cfg) {
+    set_error("null argument");
+    return HLM_B200_ERR_INPUT;
+  }
+  // check_noise_interval (weight_stream.hpp:96-100); NaNs fail it like they do in the reference
+  if (st->noise_low < 0.0 || st->noise_high < st->noise_low) {
+    set_error("noise interval must satisfy 0 <= low <= high, got [%f, %f)", st->noise_low, st->noise_high);
+    return HLM_B200_ERR_INPUT;
+  }
+  if (st->kind < 0 || st->kind > 2 || st->mode < 0 || st->mode > 1) {
+    set_error("unknown generator kind %d / weight mode %d", st->kind, st->mode);
+    return HLM_B200_ERR_INPUT;
+  }
+  CU_CHECK(cudaSetDevice(g->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  switch (cfg->variant) {
+    case HLM_B200_VARIANT_CRCW:
+      rc = match_crcw(g, st, cfg, out);
+      break;
+    case HLM_B200_VARIANT_CREW:
+      rc = match_crew(g, st, cfg, out);
+      break;
+    case HLM_B200_VARIANT_SEQ:
+    case HLM_B200_VARIANT_WORK_OPTIMAL:
+    case HLM_B200_VARIANT_GREEDY:
+      set_error("variant %d is not implemented on the device (crcw = 1 and crew = 2 are)", cfg->variant);
+      return HLM_B200_ERR_UNSUPPORTED;
+    default:
+      set_error("unknown variant %d", cfg->variant);  // local_max_par.hpp:615
+      return HLM_B200_ERR_INPUT;
+  }
+  out->wall_time_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// verify_matching (exact.hpp:115-140)
+// ---------------------------------------------------------------------------------------------
+static int verify(Graph* g, const uint32_t* matched, uint64_t count, int* disjoint, int* maximal,
+                  double* weight) {
+  CU_CHECK(cudaSetDevice(g->device));
+  cudaStream_t s = g->stream;
+  uint32_t *d_ids = nullptr, *covered = nullptr, *inm = nullptr;
+  VerifyOut* d_out = nullptr;
+  double* d_w = nullptr;
+  const size_t cw = (static_cast<size_t>(g->n) + 31) / 32, mw = (static_cast<size_t>(g->m) + 31) / 32;
+  int rc = HLM_B200_OK;
+  std::vector<double> wts;
+  VerifyOut vo = {0, 0, 0, 0};
+  auto body = [&]() -> int {
+    ST_CHECK(dev_alloc(&d_ids, count, nullptr));
+    ST_CHECK(dev_alloc(&covered, cw, nullptr));
+    ST_CHECK(dev_alloc(&inm, mw, nullptr));
+    ST_CHECK(dev_alloc(&d_out, 1, nullptr));
+    CU_CHECK(cudaMemcpyAsync(d_ids, matched, count * 4, cudaMemcpyHostToDevice, s));
+    CU_CHECK(cudaMemsetAsync(covered, 0, cw * 4, s));
+    CU_CHECK(cudaMemsetAsync(inm, 0, mw * 4, s));
+    CU_CHECK(cudaMemsetAsync(d_out, 0, sizeof(VerifyOut), s));
+    if (count)
+      k_verify_cover<<<grid_for(g, count, kWarpsPerBlock), kBlock, 0, s>>>(g->csr(), g->m, d_ids, count,
+                                                                          covered, inm, d_out);
+    CU_CHECK(cudaMemcpyAsync(&vo, d_out, sizeof(vo), cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+    if (vo.out_of_range) {
+      set_error("matching references an edge out of range");
+      return HLM_B200_ERR_INPUT;
+    }
+    if (g->m) k_verify_maximal<<<grid_for(g, g->m), kBlock, 0, s>>>(g->csr(), g->m, covered, inm, d_out);
+    if (g->base && count) {
+      ST_CHECK(dev_alloc(&d_w, count, nullptr));
+      k_gather_weights<<<grid_for(g, count), kBlock, 0, s>>>(g->base, d_ids, count, d_w);
+      wts.resize(count);
+      CU_CHECK(cudaMemcpyAsync(wts.data(), d_w, count * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CU_CHECK(cudaMemcpyAsync(&vo, d_out, sizeof(vo), cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+    CU_CHECK(cudaGetLastError());
+    return HLM_B200_OK;
+  };
+  rc = body();
+  dev_free(d_ids);
+  dev_free(covered);
+  dev_free(inm);
+  dev_free(d_out);
+  dev_free(d_w);
+  if (rc != HLM_B200_OK) return rc;
+  *disjoint = vo.overlap ? 0 : 1;
+  *maximal = vo.addable ? 0 : 1;
+  double tw = 0.0;  // accumulated in the order given, like exact.hpp:126
+  if (g->base)
+    for (uint64_t i = 0; i < count; ++i) tw += wts[i];
+  else
+    for (uint64_t i = 0; i < count; ++i) tw += g->base_const;
+  *weight = tw;
+  return HLM_B200_OK;
+}
+
+}  // namespace hlmb
+
+// ---------------------------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------------------------
+using namespace hlmb;
+
+extern "C" {
+
+int hlm_b200_abi_version(void) { return HLM_B200_ABI_VERSION; }
+
+const char* hlm_b200_last_error(void) { return g_last_error.c_str(); }
+
+int hlm_b200_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+uint32_t hlm_b200_default_max_rounds(uint32_t num_edges) { return default_max_rounds(num_edges); }
+
+int hlm_b200_graph_upload(const hlm_b200_csr_view* host, int device, hlm_b200_graph** out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  Graph* g = nullptr;
+  int rc = upload(host, device, &g);
+  *out = reinterpret_cast<hlm_b200_graph*>(g);
+  return rc;
+}
+
+int hlm_b200_graph_generate(const hlm_b200_syn_spec* spec, int device, hlm_b200_graph** out) {
+  if (!out || !spec) return HLM_B200_ERR_INPUT;
+  Graph* g = nullptr;
+  int rc = generate(spec, device, &g);
+  *out = reinterpret_cast<hlm_b200_graph*>(g);
+  return rc;
+}
+
+int hlm_b200_graph_info_get(const hlm_b200_graph* gh, hlm_b200_graph_info* info) {
+  if (!gh || !info) return HLM_B200_ERR_INPUT;
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  info->num_vertices = g->n;
+  info->num_edges = g->m;
+  info->num_pins = g->kappa;
+  info->uniform_size = g->uniform_d;
+  info->max_edge_size = g->max_edge_size;
+  info->num_large_edges = g->num_large;
+  info->unit_weights = g->base == nullptr;
+  info->device = g->device;
+  info->device_bytes = g->device_bytes;
+  return HLM_B200_OK;
+}
+
+int hlm_b200_graph_download(hlm_b200_graph* gh, uint64_t* vertex_offsets, uint32_t* vertex_incidence,
+                            uint64_t* edge_offsets, uint32_t* edge_members, double* base_weights) {
+  if (!gh) return HLM_B200_ERR_INPUT;
+  return download(reinterpret_cast<Graph*>(gh), vertex_offsets, vertex_incidence, edge_offsets,
+                  edge_members, base_weights);
+}
+
+void hlm_b200_graph_release(hlm_b200_graph* g) { delete reinterpret_cast<Graph*>(g); }
+
+int hlm_b200_match(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
+                   hlm_b200_result* out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  return run_match(reinterpret_cast<Graph*>(g), stream, cfg, out);
+}
+
+int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* stream,
+                        const hlm_b200_config* cfg, int device, hlm_b200_result* out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  std::memset(out, 0, sizeof(*out));
+  Graph* g = nullptr;
+  int rc = upload(host, device, &g);
+  if (rc != HLM_B200_OK) return rc;
+  rc = run_match(g, stream, cfg, out);
+  delete g;
+  return rc;
+}
+
+void hlm_b200_result_free(hlm_b200_result* r) {
+  if (!r) return;
+  std::free(r->matched_edges);
+  std::free(r->matched_round);
+  std::free(r->per_round_matched);
+  std::free(r->per_round_deactivated);
+  std::memset(r, 0, sizeof(*r));
+}
+
+int hlm_b200_verify(hlm_b200_graph* g, const uint32_t* matched, uint64_t count, int* disjoint,
+                    int* maximal, double* weight) {
+  if (!g || (!matched && count) || !disjoint || !maximal || !weight) return HLM_B200_ERR_INPUT;
+  return verify(reinterpret_cast<Graph*>(g), matched, count, disjoint, maximal, weight);
+}
+
+int hlm_b200_eval_stream(const hlm_b200_stream* st, const uint32_t* edges, const uint32_t* rounds,
+                         const double* base, size_t count, double* w_out, uint64_t* t_out, int device) {
+  if (!st || !edges || !rounds || !w_out || !t_out) return HLM_B200_ERR_INPUT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device available; libhlm_b200 has no CPU fallback");
+    return HLM_B200_ERR_CUDA;
+  }
+  CU_CHECK(cudaSetDevice(device));
+  StreamParams sp;
+  sp.seed = st->seed;
+  sp.kind = st->kind;
+  sp.mode = st->mode;
+  sp.lo = st->noise_low;
+  sp.hi = st->noise_high;
+  sp.width = st->noise_high - st->noise_low;
+  uint32_t *d_e = nullptr, *d_r = nullptr;
+  double *d_b = nullptr, *d_w = nullptr;
+  unsigned long long* d_t = nullptr;
+  auto body = [&]() -> int {
+    ST_CHECK(dev_alloc(&d_e, count, nullptr));
+    ST_CHECK(dev_alloc(&d_r, count, nullptr));
+    ST_CHECK(dev_alloc(&d_w, count, nullptr));
+    ST_CHECK(dev_alloc(&d_t, count, nullptr));
+    CU_CHECK(cudaMemcpy(d_e, edges, count * 4, cudaMemcpyHostToDevice));
+    CU_CHECK(cudaMemcpy(d_r, rounds, count * 4, cudaMemcpyHostToDevice));
+    if (base) {
+      ST_CHECK(dev_alloc(&d_b, count, nullptr));
+      CU_CHECK(cudaMemcpy(d_b, base, count * 8, cudaMemcpyHostToDevice));
+    }
+    if (count) {
+      const int grid = static_cast<int>(std::min<size_t>((count + kBlock - 1) / kBlock, 4096));
+      k_eval_stream<<<grid, kBlock>>>(sp, d_e, d_r, d_b, count, d_w, d_t);
+    }
+    CU_CHECK(cudaMemcpy(w_out, d_w, count * 8, cudaMemcpyDeviceToHost));
+    CU_CHECK(cudaMemcpy(t_out, d_t, count * 8, cudaMemcpyDeviceToHost));
+    CU_CHECK(cudaGetLastError());
+    return HLM_B200_OK;
+  };
+  const int rc = body();
+  dev_free(d_e);
+  dev_free(d_r);
+  dev_free(d_b);
+  dev_free(d_w);
+  dev_free(d_t);
+  return rc;
+}
+
+}  // extern "C"

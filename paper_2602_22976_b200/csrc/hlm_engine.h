@@ -1,0 +1,94 @@
+// hlm_engine.h -- host-side types shared by the translation units of libhlm_b200.so.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hlm_b200.h"
+#include "hlm_types.cuh"
+
+namespace hlmb {
+
+struct Graph;
+
+// Per-instance scratch in HBM, allocated on the first match and reused by later ones.
+struct Workspace {
+  Ctrl* ctrl = nullptr;
+  unsigned long long* vkey = nullptr;
+  uint32_t* dead = nullptr;
+  uint16_t* mround = nullptr;
+  uint32_t* list[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint8_t* mflag[2] = {nullptr, nullptr};
+  uint32_t* matched_cnt = nullptr;
+  uint32_t* deact_cnt = nullptr;
+  uint32_t rounds_cap = 0;
+  // exact tie path
+  unsigned long long* va = nullptr;
+  unsigned long long* vb = nullptr;
+  uint32_t* vc = nullptr;
+  // result assembly
+  uint32_t* chunk_cnt = nullptr;
+  uint32_t num_chunks = 0;
+  unsigned long long* scan_total = nullptr;
+  uint32_t* out_ids = nullptr;
+  uint16_t* out_round = nullptr;
+  double* out_w = nullptr;
+  uint64_t out_cap = 0;
+  // CUDA-graph WHILE loop over the round body
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  RoundParams graph_key = {};
+  uint32_t graph_body_launches = 0;
+  uint32_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void release();
+};
+
+struct CrewState;  // hlm_crew.cu
+
+// An instance resident in HBM (pin-CSR as 32-bit arrays, optional incidence-CSR).
+struct Graph {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  uint32_t n = 0, m = 0;
+  uint32_t id_base = 0;  // global id of local edge 0 (edge shard of a larger instance)
+  uint64_t kappa = 0;
+  uint32_t* pins = nullptr;
+  uint32_t* off32 = nullptr;
+  uint64_t* off64 = nullptr;
+  uint32_t uniform_d = 0;
+  uint32_t max_edge_size = 0;
+  uint32_t num_large = 0;
+  uint32_t* large_list = nullptr;
+  double* base = nullptr;  // null: all weights equal base_const
+  double base_const = 1.0;
+  double base_min = 1.0, base_max = 1.0;
+  // vertex -> incident edges, built on the device when a variant (crew) or a download needs it
+  uint64_t* voff = nullptr;  // n+1
+  uint32_t* vinc = nullptr;  // kappa
+  uint64_t device_bytes = 0;
+  uint64_t h2d_bytes = 0;
+  int round_grid = 0, large_grid = 0;
+  Workspace ws;
+  CrewState* crew = nullptr;
+  EdgeCsr csr() const;
+  ~Graph();
+};
+
+void set_error(const char* fmt, ...);
+uint32_t default_max_rounds(uint32_t m);
+int new_graph(int device, Graph** out);
+int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins);
+int finish_weights(Graph* g);
+int weight_stats(Graph* g, double lo, WeightStats* out);
+int build_incidence(Graph* g);
+int generate(const hlm_b200_syn_spec* spec, int device, Graph** out);
+int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base);
+int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);
+void crew_release(Graph* g);
+int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
+                    hlm_b200_result* out);
+int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out, uint64_t count,
+                                     uint64_t* total);
+
+}  // namespace hlmb

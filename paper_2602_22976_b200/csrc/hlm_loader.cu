@@ -1,0 +1,464 @@
+// hlm_loader.cu -- device-side instance sources and CSR utilities of libhlm_b200.so:
+//   * counter-based synthetic generators (the BASELINE.json configs 2-5; definitions in
+//     DESIGN.md "Synthetic instances", CPU restatement in oracle/hlm_oracle.c orc_syn_*),
+//   * the vertex-incidence CSR builder (counting sort of pins by vertex; the device analogue of
+//     hypergraph.hpp:144-151),
+//   * exclusive scan, download.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "hlm_engine.h"
+
+namespace hlmb {
+
+#define CU_CHECK(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return HLM_B200_ERR_CUDA;                                                            \
+    }                                                                                      \
+  } while (0)
+#define ST_CHECK(expr)                \
+  do {                                \
+    int _s = (expr);                  \
+    if (_s != HLM_B200_OK) return _s; \
+  } while (0)
+
+template <typename T>
+static int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HLM_B200_ERR_NOMEM : HLM_B200_ERR_CUDA;
+  }
+  return HLM_B200_OK;
+}
+
+static int grid_of(const Graph* g, uint64_t items, int per_block = kBlock) {
+  const uint64_t want = (items + per_block - 1) / per_block;
+  const uint64_t cap = static_cast<uint64_t>(g->num_sms) * 8;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+// ---------------------------------------------------------------------------------------------
+// exclusive scan u32 -> u64 (three passes: chunk sums, one-block scan of the sums, rescan)
+// ---------------------------------------------------------------------------------------------
+constexpr int kScanItems = 16;
+constexpr uint32_t kScanChunk = kBlock * kScanItems;
+
+__global__ void __launch_bounds__(kBlock) k_scan_chunk_sums(const uint32_t* in, uint64_t count,
+                                                            unsigned long long* sums) {
+  __shared__ unsigned long long s_w[kWarpsPerBlock];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk + threadIdx.x * kScanItems;
+  unsigned long long acc = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < count) acc += in[base + k];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kWarpsPerBlock; ++w) t += s_w[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(unsigned long long* vals, uint64_t cnt,
+                                                    unsigned long long* total) {
+  __shared__ unsigned long long s_part[1024];
+  const uint64_t per = (cnt + 1023) / 1024;
+  const uint64_t b = threadIdx.x * per;
+  const uint64_t e = min(cnt, b + per);
+  unsigned long long acc = 0;
+  for (uint64_t i = b; i < e; ++i) acc += vals[i];
+  s_part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const unsigned long long v = s_part[i];
+      s_part[i] = run;
+      run += v;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  unsigned long long run = s_part[threadIdx.x];
+  for (uint64_t i = b; i < e; ++i) {
+    const unsigned long long v = vals[i];
+    vals[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_scan_write(const uint32_t* in, uint64_t count,
+                                                       const unsigned long long* sums,
+                                                       unsigned long long* out) {
+  __shared__ unsigned long long s_w[kWarpsPerBlock];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk + threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  unsigned long long acc = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = base + k < count ? in[base + k] : 0u;
+    acc += v[k];
+  }
+  // exclusive prefix of the per-thread totals across the block
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = acc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += t;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  unsigned long long before = sums[blockIdx.x];
+  for (uint32_t w = 0; w < warp; ++w) before += s_w[w];
+  unsigned long long run = before + incl - acc;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < count) out[base + k] = run;
+    run += v[k];
+  }
+}
+
+// out has count+1 entries; out[count] = total.
+int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out, uint64_t count,
+                                     uint64_t* total) {
+  cudaStream_t s = g->stream;
+  const uint64_t chunks = (count + kScanChunk - 1) / kScanChunk;
+  unsigned long long* sums = nullptr;
+  ST_CHECK(dalloc(&sums, chunks + 1));
+  uint64_t tot = 0;
+  if (count) {
+    k_scan_chunk_sums<<<static_cast<unsigned>(chunks), kBlock, 0, s>>>(in, count, sums);
+    k_scan_sums<<<1, 1024, 0, s>>>(sums, chunks, sums + chunks);
+    k_scan_write<<<static_cast<unsigned>(chunks), kBlock, 0, s>>>(
+        in, count, sums, reinterpret_cast<unsigned long long*>(out));
+    CU_CHECK(cudaMemcpyAsync(&tot, sums + chunks, 8, cudaMemcpyDeviceToHost, s));
+  }
+  CU_CHECK(cudaStreamSynchronize(s));
+  CU_CHECK(cudaMemcpyAsync(out + count, &tot, 8, cudaMemcpyHostToDevice, s));
+  CU_CHECK(cudaStreamSynchronize(s));
+  cudaFree(sums);
+  CU_CHECK(cudaGetLastError());
+  if (total) *total = tot;
+  return HLM_B200_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// vertex-incidence CSR (order inside one vertex's list is unspecified; no matcher depends on it)
+// ---------------------------------------------------------------------------------------------
+__global__ void k_degree(const uint32_t* pins, uint64_t kappa, uint32_t* deg) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < kappa;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(deg + pins[i], 1u);
+}
+
+__global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, const unsigned long long* voff,
+                                 uint32_t* cursor, uint32_t* vinc) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    uint64_t b;
+    uint32_t s;
+    csr.range(e, b, s);
+    for (uint32_t i = 0; i < s; ++i) {
+      const uint32_t v = csr.pins[b + i];
+      vinc[voff[v] + atomicAdd(cursor + v, 1u)] = e;
+    }
+  }
+}
+
+int build_incidence(Graph* g) {
+  if (g->voff) return HLM_B200_OK;
+  cudaStream_t s = g->stream;
+  uint32_t* deg = nullptr;
+  ST_CHECK(dalloc(&deg, g->n));
+  ST_CHECK(dalloc(&g->voff, static_cast<size_t>(g->n) + 1));
+  ST_CHECK(dalloc(&g->vinc, g->kappa));
+  g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
+  CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
+  if (g->kappa) k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, deg);
+  int rc = device_exclusive_scan_u32_to_u64(g, deg, g->voff, g->n, nullptr);
+  if (rc != HLM_B200_OK) {
+    cudaFree(deg);
+    return rc;
+  }
+  CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
+  if (g->m)
+    k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(
+        g->csr(), g->m, reinterpret_cast<const unsigned long long*>(g->voff), deg, g->vinc);
+  CU_CHECK(cudaStreamSynchronize(s));
+  cudaFree(deg);
+  CU_CHECK(cudaGetLastError());
+  return HLM_B200_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// synthetic instances
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t syn_hash(uint64_t seed, uint64_t tag, uint64_t e, uint64_t k) {
+  return mix_splitmix(mix_splitmix(mix_splitmix(seed + tag) + e) + k);
+}
+
+struct SynParams {
+  int32_t family;
+  uint32_t n, d, scale;
+  uint64_t seed;
+  uint32_t edge_begin;  // global id of local edge 0
+  uint32_t m_local;
+  unsigned long long size_total;  // POWERLAW: sum of floor(2^40 / s^2), s = 2..64
+};
+
+__device__ __forceinline__ uint32_t syn_edge_size(const SynParams& p, uint32_t e) {
+  if (p.family == HLM_B200_SYN_UNIFORM) return p.d;
+  if (p.family == HLM_B200_SYN_RMAT) return 2;
+  if (p.family == HLM_B200_SYN_POWERLAW) {
+    unsigned long long x = syn_hash(p.seed, 1, e, 0) % p.size_total;
+    for (unsigned long long s = 2; s <= 64; ++s) {
+      const unsigned long long w = (1ull << 40) / (s * s);
+      if (x < w) return static_cast<uint32_t>(s);
+      x -= w;
+    }
+    return 64;
+  }
+  const uint64_t c = syn_hash(p.seed, 1, e, 0);
+  if (c % 1000 == 0) {
+    const uint32_t o = static_cast<uint32_t>((c >> 10) % 6);
+    const uint32_t f = static_cast<uint32_t>((c >> 16) % (64u << o));
+    uint32_t s = (64u << o) + f + 1;
+    return s > p.n ? p.n : s;
+  }
+  const uint64_t gg = (c >> 10) & 0xFFFFFFFFull;
+  uint64_t q = 1ull << 32;
+  uint32_t k = 0;
+  while (k < 30) {
+    q = q * 3 / 5;
+    if (gg >= q) break;
+    ++k;
+  }
+  const uint32_t s = 2 + k;
+  return s > p.n ? p.n : s;
+}
+
+__device__ __forceinline__ uint32_t syn_draw_vertex(const SynParams& p, uint32_t e, uint32_t j, uint32_t a) {
+  const uint64_t h = syn_hash(p.seed, 2, e, (static_cast<uint64_t>(j) << 32) | a);
+  if (p.family == HLM_B200_SYN_POWERLAW) {
+    const uint64_t u = h >> 32;
+    const uint64_t t1 = (u * u) >> 32;
+    const uint64_t t2 = (t1 * u) >> 32;
+    return static_cast<uint32_t>((t2 * static_cast<uint64_t>(p.n)) >> 32);
+  }
+  return static_cast<uint32_t>(__umul64hi(h, static_cast<uint64_t>(p.n)));
+}
+
+__global__ void k_syn_sizes(const SynParams p, uint32_t* sizes) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m_local; i += gridDim.x * blockDim.x)
+    sizes[i] = syn_edge_size(p, p.edge_begin + i);
+}
+
+// one thread per edge; `off` null means uniform size p.d (or 2 for RMAT)
+__global__ void k_syn_pins(const SynParams p, const unsigned long long* off, uint32_t* pins) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m_local; i += gridDim.x * blockDim.x) {
+    const uint32_t e = p.edge_begin + i;
+    if (p.family == HLM_B200_SYN_RMAT) {
+      uint32_t u = 0, v = 0;
+      for (uint32_t a = 0;; ++a) {
+        u = 0;
+        v = 0;
+        uint64_t h = 0;
+        for (uint32_t lvl = 0; lvl < p.scale; ++lvl) {
+          if ((lvl & 3) == 0) h = syn_hash(p.seed, 2, e, (static_cast<uint64_t>(a) << 32) | (lvl >> 2));
+          const uint32_t r = static_cast<uint32_t>((h >> (16 * (lvl & 3))) & 0xFFFFu);
+          const uint32_t bu = r >= 49807u;
+          const uint32_t bv = (r >= 37356u && r < 49807u) || r >= 62259u;
+          u = (u << 1) | bu;
+          v = (v << 1) | bv;
+        }
+        if (u != v) break;
+      }
+      reinterpret_cast<uint2*>(pins)[i] = make_uint2(u, v);
+      continue;
+    }
+    uint64_t b;
+    uint32_t s;
+    if (off) {
+      b = off[i];
+      s = static_cast<uint32_t>(off[i + 1] - b);
+    } else {
+      b = static_cast<uint64_t>(i) * p.d;
+      s = p.d;
+    }
+    uint32_t* pp = pins + b;
+    for (uint32_t j = 0; j < s; ++j) {
+      for (uint32_t a = 0;; ++a) {
+        const uint32_t v = syn_draw_vertex(p, e, j, a);
+        bool seen = false;
+        for (uint32_t q = 0; q < j; ++q) seen |= (pp[q] == v);
+        if (!seen) {
+          pp[j] = v;
+          break;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_syn_weights(const SynParams p, double* base) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m_local; i += gridDim.x * blockDim.x)
+    base[i] = static_cast<double>(1 + syn_hash(p.seed, 3, p.edge_begin + i, 0) % 100);
+}
+
+int generate(const hlm_b200_syn_spec* spec, int device, Graph** out) {
+  *out = nullptr;
+  const uint32_t n = spec->family == HLM_B200_SYN_RMAT ? (spec->scale < 32 ? 1u << spec->scale : 0u) : spec->n;
+  if (spec->family < 0 || spec->family > 3 || n < 2 || spec->m == 0 ||
+      (spec->family == HLM_B200_SYN_UNIFORM && (spec->d == 0 || spec->d > n || spec->d > 4096))) {
+    set_error("bad synthetic instance spec");
+    return HLM_B200_ERR_INPUT;
+  }
+  uint32_t begin = spec->edge_begin, m_local = spec->m_local;
+  if (begin == 0 && m_local == 0) m_local = spec->m;
+  if (static_cast<uint64_t>(begin) + m_local > spec->m) {
+    set_error("edge shard [%u, %u + %u) exceeds m = %u", begin, begin, m_local, spec->m);
+    return HLM_B200_ERR_INPUT;
+  }
+  Graph* g = nullptr;
+  ST_CHECK(new_graph(device, &g));
+  auto fail = [&](int rc) {
+    delete g;
+    return rc;
+  };
+  cudaStream_t s = g->stream;
+  g->n = n;
+  g->m = m_local;
+  g->id_base = begin;
+  SynParams p;
+  p.family = spec->family;
+  p.n = n;
+  p.d = spec->d;
+  p.scale = spec->scale;
+  p.seed = spec->seed;
+  p.edge_begin = begin;
+  p.m_local = m_local;
+  p.size_total = 0;
+  for (unsigned long long q = 2; q <= 64; ++q) p.size_total += (1ull << 40) / (q * q);
+
+  int rc;
+  const bool uniform = spec->family == HLM_B200_SYN_UNIFORM || spec->family == HLM_B200_SYN_RMAT;
+  uint64_t* off64 = nullptr;
+  if ((rc = dalloc(&off64, static_cast<size_t>(m_local) + 1)) != HLM_B200_OK) return fail(rc);
+  if (uniform) {
+    const uint32_t d = spec->family == HLM_B200_SYN_RMAT ? 2u : spec->d;
+    p.d = d;
+    g->kappa = static_cast<uint64_t>(m_local) * d;
+    if ((rc = dalloc(&g->pins, g->kappa)) != HLM_B200_OK) return fail(rc);
+    g->device_bytes += g->kappa * 4;
+    k_syn_pins<<<grid_of(g, m_local), kBlock, 0, s>>>(p, nullptr, g->pins);
+    // uniform instances never materialise offsets
+    cudaFree(off64);
+    g->uniform_d = d;
+    g->max_edge_size = d;
+    g->num_large = d > kLargeEdge ? m_local : 0;
+    if (g->num_large) {
+      set_error("uniform synthetic instances support d <= %u", kLargeEdge);
+      return fail(HLM_B200_ERR_UNSUPPORTED);
+    }
+  } else {
+    uint32_t* sizes = nullptr;
+    if ((rc = dalloc(&sizes, m_local)) != HLM_B200_OK) return fail(rc);
+    k_syn_sizes<<<grid_of(g, m_local), kBlock, 0, s>>>(p, sizes);
+    rc = device_exclusive_scan_u32_to_u64(g, sizes, off64, m_local, &g->kappa);
+    cudaFree(sizes);
+    if (rc != HLM_B200_OK) {
+      cudaFree(off64);
+      return fail(rc);
+    }
+    if ((rc = dalloc(&g->pins, g->kappa)) != HLM_B200_OK) {
+      cudaFree(off64);
+      return fail(rc);
+    }
+    g->device_bytes += g->kappa * 4;
+    k_syn_pins<<<grid_of(g, m_local), kBlock, 0, s>>>(
+        p, reinterpret_cast<const unsigned long long*>(off64), g->pins);
+    if ((rc = finish_graph(g, off64, false)) != HLM_B200_OK) return fail(rc);
+  }
+  if (spec->int_weights) {
+    if ((rc = dalloc(&g->base, m_local)) != HLM_B200_OK) return fail(rc);
+    g->device_bytes += static_cast<uint64_t>(m_local) * 8;
+    k_syn_weights<<<grid_of(g, m_local), kBlock, 0, s>>>(p, g->base);
+    if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
+  } else {
+    g->base = nullptr;
+    g->base_const = g->base_min = g->base_max = 1.0;
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("synthetic generation failed: %s", cudaGetErrorString(e));
+    return fail(HLM_B200_ERR_CUDA);
+  }
+  *out = g;
+  return HLM_B200_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// download
+// ---------------------------------------------------------------------------------------------
+__global__ void k_widen_offsets(const EdgeCsr csr, uint32_t m, unsigned long long* out) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e <= m;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (csr.uniform_d)
+      out[e] = e * csr.uniform_d;
+    else if (csr.off32)
+      out[e] = csr.off32[e];
+    else
+      out[e] = csr.off64[e];
+  }
+}
+
+__global__ void k_fill_const(double* out, uint32_t m, double v) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) out[e] = v;
+}
+
+int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base) {
+  CU_CHECK(cudaSetDevice(g->device));
+  cudaStream_t s = g->stream;
+  if (eoff) {
+    unsigned long long* tmp = nullptr;
+    ST_CHECK(dalloc(&tmp, static_cast<size_t>(g->m) + 1));
+    k_widen_offsets<<<grid_of(g, g->m + 1ull), kBlock, 0, s>>>(g->csr(), g->m, tmp);
+    CU_CHECK(cudaMemcpyAsync(eoff, tmp, (static_cast<size_t>(g->m) + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+  }
+  if (pins && g->kappa) CU_CHECK(cudaMemcpyAsync(pins, g->pins, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+  if (base && g->m) {
+    if (g->base) {
+      CU_CHECK(cudaMemcpyAsync(base, g->base, static_cast<size_t>(g->m) * 8, cudaMemcpyDeviceToHost, s));
+    } else {
+      double* tmp = nullptr;
+      ST_CHECK(dalloc(&tmp, g->m));
+      k_fill_const<<<grid_of(g, g->m), kBlock, 0, s>>>(tmp, g->m, g->base_const);
+      CU_CHECK(cudaMemcpyAsync(base, tmp, static_cast<size_t>(g->m) * 8, cudaMemcpyDeviceToHost, s));
+      CU_CHECK(cudaStreamSynchronize(s));
+      cudaFree(tmp);
+    }
+  }
+  if (voff || vinc) {
+    ST_CHECK(build_incidence(g));
+    if (voff)
+      CU_CHECK(cudaMemcpyAsync(voff, g->voff, (static_cast<size_t>(g->n) + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (vinc && g->kappa)
+      CU_CHECK(cudaMemcpyAsync(vinc, g->vinc, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CU_CHECK(cudaStreamSynchronize(s));
+  CU_CHECK(cudaGetLastError());
+  return HLM_B200_OK;
+}
+
+}  // namespace hlmb
