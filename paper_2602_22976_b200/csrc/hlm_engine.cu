@@ -89,9 +89,12 @@ void Workspace::release() {
   dev_free(vkey);
   dev_free(dead);
   dev_free(mround);
-  for (int c = 0; c < 2; ++c) {
-    for (int b = 0; b < 2; ++b) dev_free(list[c][b]);
-    dev_free(mflag[c]);
+  dev_free(mbits);
+  for (int b = 0; b < 2; ++b) {
+    dev_free(seg_ids[b]);
+    dev_free(seg_cnt[b]);
+    dev_free(list1[b]);
+    dev_free(mflag[b]);
   }
   dev_free(matched_cnt);
   dev_free(deact_cnt);
@@ -103,6 +106,10 @@ void Workspace::release() {
   dev_free(out_ids);
   dev_free(out_round);
   dev_free(out_w);
+  dev_free(int_sum);
+  if (pin_ids) cudaFreeHost(pin_ids);
+  if (pin_round) cudaFreeHost(pin_round);
+  if (pin_w) cudaFreeHost(pin_w);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (graph) cudaGraphDestroy(graph);
   if (ev0) cudaEventDestroy(ev0);
@@ -229,6 +236,7 @@ int finish_weights(Graph* g) {
   }
   std::memcpy(&g->base_min, &ws.min_bits, 8);
   std::memcpy(&g->base_max, &ws.max_bits, 8);
+  g->base_integral = !ws.non_integer;
   if (ws.min_bits == ws.max_bits) {
     g->base_const = g->base_min;
     cudaFree(g->base);
@@ -323,15 +331,25 @@ static int ensure_workspace(Graph* g, uint32_t max_rounds) {
     ST_CHECK(dev_alloc(&w.vkey, g->n, g));
     ST_CHECK(dev_alloc(&w.dead, (static_cast<size_t>(g->n) + 31) / 32, g));
     ST_CHECK(dev_alloc(&w.mround, g->m, g));
+    w.mbits_words = (g->m + 31) / 32;
+    ST_CHECK(dev_alloc(&w.mbits, w.mbits_words, g));
+    // class-0 lists: regions of seg_cap edge ids, several regions per resident CTA so that the
+    // ticket scheduler can balance uneven survivor counts
+    const uint32_t target = static_cast<uint32_t>(g->num_sms) * 64u;
+    w.seg_cap = std::max<uint32_t>(1024u, (g->m + target - 1) / std::max(1u, target));
+    w.seg_cap = (w.seg_cap + 1023u) / 1024u * 1024u;
+    w.nseg = std::max<uint32_t>(1u, (g->m + w.seg_cap - 1) / w.seg_cap);
     for (int b = 0; b < 2; ++b) {
-      ST_CHECK(dev_alloc(&w.list[0][b], g->m, g));
-      ST_CHECK(dev_alloc(&w.list[1][b], g->num_large, g));
+      ST_CHECK(dev_alloc(&w.seg_ids[b], static_cast<size_t>(w.nseg) * w.seg_cap, g));
+      ST_CHECK(dev_alloc(&w.seg_cnt[b], w.nseg, g));
+      ST_CHECK(dev_alloc(&w.list1[b], g->num_large, g));
     }
-    ST_CHECK(dev_alloc(&w.mflag[0], g->m, g));
+    ST_CHECK(dev_alloc(&w.mflag[0], static_cast<size_t>(w.nseg) * w.seg_cap, g));
     ST_CHECK(dev_alloc(&w.mflag[1], g->num_large, g));
-    w.num_chunks = (g->m + kAsmChunk - 1) / kAsmChunk;
+    w.num_chunks = (w.mbits_words + kAsmChunkWords - 1) / kAsmChunkWords;
     ST_CHECK(dev_alloc(&w.chunk_cnt, w.num_chunks, g));
     ST_CHECK(dev_alloc(&w.scan_total, 1, g));
+    ST_CHECK(dev_alloc(&w.int_sum, 1, g));
     CU_CHECK(cudaEventCreate(&w.ev0));
     CU_CHECK(cudaEventCreate(&w.ev1));
   }
@@ -462,20 +480,21 @@ static int exact_round(Launcher& L, uint32_t r, uint32_t buf, const Ctrl& c) {
   CU_CHECK(cudaMemsetAsync(w.vb, 0, static_cast<size_t>(g->n) * 8, s));
   CU_CHECK(cudaMemsetAsync(w.vc, 0, static_cast<size_t>(g->n) * 4, s));
   ExactParams X[2];
-  for (int cls = 0; cls < 2; ++cls) {
+  for (uint32_t cls = 0; cls < 2; ++cls) {
     X[cls].va = w.va;
     X[cls].vb = w.vb;
     X[cls].vc = w.vc;
-    X[cls].list = (cls == 0 && L.P.ident0 && r == 1) ? nullptr : w.list[cls][buf];
-    X[cls].count = c.count[buf][cls];
     X[cls].round = r;
     X[cls].cls = cls;
-    X[cls].mflag = w.mflag[cls];
+    X[cls].buf = buf;
+    X[cls].ident = r == 1;
+    X[cls].count1 = c.count1[buf];
   }
-  auto level = [&](int lv) {
+  const uint64_t slots[2] = {static_cast<uint64_t>(w.nseg) * w.seg_cap, c.count1[buf]};
+  for (int lv = 1; lv <= 4; ++lv) {
     for (int cls = 0; cls < 2; ++cls) {
-      if (X[cls].count == 0) continue;
-      const int grid = grid_for(g, X[cls].count, kWarpsPerBlock);
+      if (slots[cls] == 0) continue;
+      const int grid = grid_for(g, slots[cls], kWarpsPerBlock);
       switch (lv) {
         case 1: k_exact_level<1><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
         case 2: k_exact_level<2><<<grid, kBlock, 0, s>>>(L.P, X[cls]); break;
@@ -484,8 +503,7 @@ static int exact_round(Launcher& L, uint32_t r, uint32_t buf, const Ctrl& c) {
       }
       ++L.launches;
     }
-  };
-  for (int lv = 1; lv <= 4; ++lv) level(lv);
+  }
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
 }
@@ -536,9 +554,6 @@ static bool same_params(const RoundParams& a, const RoundParams& b) {
   return std::memcmp(&a, &b, sizeof(RoundParams)) == 0;
 }
 
-int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);
-int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant, hlm_b200_result* out);
-
 int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
   const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
   if (max_rounds > 65000u) {
@@ -568,15 +583,23 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   P.stream.hi = st->noise_high;
   P.stream.width = st->noise_high - st->noise_low;
   ST_CHECK(choose_key_scheme(g, P.stream, max_rounds, &P.ks));
+  // the load-before-atomic filter pays off once a vertex sees many edges per round
+  P.ks.precheck = (g->n && g->kappa / g->n >= 6) ? 1u : 0u;
+  if (const char* env = std::getenv("HLM_B200_PRECHECK")) P.ks.precheck = env[0] == '1';
   P.ctrl = w.ctrl;
   P.vkey = w.vkey;
   P.dead = w.dead;
+  P.mbits = w.mbits;
   P.mround = w.mround;
-  for (int c = 0; c < 2; ++c) {
-    for (int b = 0; b < 2; ++b) P.list[c][b] = w.list[c][b];
-    P.mflag[c] = w.mflag[c];
+  for (int b = 0; b < 2; ++b) {
+    P.seg_ids[b] = w.seg_ids[b];
+    P.seg_cnt[b] = w.seg_cnt[b];
+    P.list1[b] = w.list1[b];
   }
-  P.ident0 = 1;
+  P.nseg = w.nseg;
+  P.seg_cap = w.seg_cap;
+  P.mflag0 = w.mflag[0];
+  P.mflag1 = w.mflag[1];
   P.matched_cnt = w.matched_cnt;
   P.deact_cnt = w.deact_cnt;
 
@@ -595,17 +618,16 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   Ctrl c0;
   std::memset(&c0, 0, sizeof(c0));
   c0.round = 1;
-  c0.count[0][0] = g->m;
-  c0.count[0][1] = g->num_large;
+  c0.count1[0] = g->num_large;
   c0.max_rounds = max_rounds;
   CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
   CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
   CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
-  CU_CHECK(cudaMemsetAsync(w.mround, 0, static_cast<size_t>(g->m) * 2, s));
+  CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
   if (g->num_large)
-    CU_CHECK(cudaMemcpyAsync(w.list[1][0], g->large_list, static_cast<size_t>(g->num_large) * 4,
+    CU_CHECK(cudaMemcpyAsync(w.list1[0], g->large_list, static_cast<size_t>(g->num_large) * 4,
                              cudaMemcpyDeviceToDevice, s));
 
   Ctrl c = c0;
@@ -642,12 +664,12 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
         CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
         CU_CHECK(cudaStreamSynchronize(s));
         if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
+        if (c.status == ST_TIE) {
+          set_error("internal: tie flag survived the exact redo");
+          return HLM_B200_ERR_CUDA;
+        }
       }
       if (c.status == ST_EPOCH) CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
-      if (c.status == ST_TIE) {
-        set_error("internal: tie flag survived the exact redo");
-        return HLM_B200_ERR_CUDA;
-      }
     }
   }
   CU_CHECK(cudaGetLastError());
@@ -655,7 +677,6 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   out->tie_redo_rounds = tie_redo;
   out->graph_launches = graph_launches;
   out->device_edge_visits = c.edges_swept;
-  w.launches = L.launches + graph_launches * w.graph_body_launches * 0;  // refined below
   // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
   out->kernel_launches = L.launches + (use_graph ? (rounds + 1) * w.graph_body_launches : 0);
   int rc = assemble_result(g, rounds, cfg, HLM_B200_VARIANT_CRCW, out);
@@ -663,7 +684,21 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
 
-// finish_matching (local_max_seq.hpp:74-83) + the RunReport counters.
+static int ensure_pinned(Workspace& w, uint64_t total, bool need_w) {
+  if (total <= w.pin_cap && (!need_w || w.pin_w)) return HLM_B200_OK;
+  if (w.pin_ids) cudaFreeHost(w.pin_ids);
+  if (w.pin_round) cudaFreeHost(w.pin_round);
+  if (w.pin_w) cudaFreeHost(w.pin_w);
+  w.pin_ids = w.pin_round = w.pin_w = nullptr;
+  w.pin_cap = total + total / 8 + 1024;
+  CU_CHECK(cudaHostAlloc(&w.pin_ids, w.pin_cap * 4, cudaHostAllocDefault));
+  CU_CHECK(cudaHostAlloc(&w.pin_round, w.pin_cap * 2, cudaHostAllocDefault));
+  if (need_w) CU_CHECK(cudaHostAlloc(&w.pin_w, w.pin_cap * 8, cudaHostAllocDefault));
+  return HLM_B200_OK;
+}
+
+// finish_matching (local_max_seq.hpp:74-83) + the RunReport counters.  Expects the matched
+// bitmap (ws.mbits) and the per-edge round record (ws.mround) to be final.
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
                     hlm_b200_result* out) {
   Workspace& w = g->ws;
@@ -671,15 +706,19 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   const uint32_t m = g->m;
   uint64_t total = 0;
   if (m) {
-    k_assemble_count<<<w.num_chunks, kBlock, 0, s>>>(w.mround, m, w.chunk_cnt);
+    k_assemble_count<<<w.num_chunks, kBlock, 0, s>>>(w.mbits, w.mbits_words, w.chunk_cnt);
     k_scan_small<<<1, 1024, 0, s>>>(w.chunk_cnt, w.num_chunks, w.scan_total);
     CU_CHECK(cudaMemcpyAsync(&total, w.scan_total, 8, cudaMemcpyDeviceToHost, s));
     CU_CHECK(cudaStreamSynchronize(s));
     out->kernel_launches += 2;
   }
   const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
-  const bool need_w = g->base != nullptr;
-  if (total > w.out_cap) {
+  // integer weights: every partial sum is an integer below 2^53, so any summation order gives
+  // the reference's ascending-id sum exactly and the device can reduce in parallel
+  const bool int_sum = g->base && g->base_integral &&
+                       g->base_max * static_cast<double>(m) < 9007199254740992.0;
+  const bool need_w = g->base != nullptr && !int_sum;
+  if (total > w.out_cap || (need_w && !w.out_w)) {
     dev_free(w.out_ids);
     dev_free(w.out_round);
     dev_free(w.out_w);
@@ -691,6 +730,7 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     ST_CHECK(dev_alloc(&w.out_round, w.out_cap, g));
     if (need_w) ST_CHECK(dev_alloc(&w.out_w, w.out_cap, g));
   }
+  ST_CHECK(ensure_pinned(w, total, need_w));
   out->num_matched = total;
   out->rounds = rounds;
   out->matched_edges = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (total + 1)));
@@ -702,19 +742,17 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     set_error("host allocation of the result failed");
     return HLM_B200_ERR_NOMEM;
   }
-  std::vector<double> wts;
+  unsigned long long isum = 0;
   if (total) {
-    k_assemble_write<<<w.num_chunks, kBlock, 0, s>>>(w.mround, m, w.chunk_cnt, g->base, g->id_base, w.out_ids,
-                                                     want_round ? w.out_round : nullptr,
-                                                     need_w ? w.out_w : nullptr);
+    if (int_sum) CU_CHECK(cudaMemsetAsync(w.int_sum, 0, 8, s));
+    k_assemble_write<<<w.num_chunks, kBlock, 0, s>>>(
+        w.mbits, w.mbits_words, w.chunk_cnt, w.mround, g->base, g->id_base, w.out_ids,
+        want_round ? w.out_round : nullptr, need_w ? w.out_w : nullptr, int_sum ? w.int_sum : nullptr);
     out->kernel_launches += 1;
-    CU_CHECK(cudaMemcpyAsync(out->matched_edges, w.out_ids, total * 4, cudaMemcpyDeviceToHost, s));
-    if (want_round)
-      CU_CHECK(cudaMemcpyAsync(out->matched_round, w.out_round, total * 2, cudaMemcpyDeviceToHost, s));
-    if (need_w) {
-      wts.resize(total);
-      CU_CHECK(cudaMemcpyAsync(wts.data(), w.out_w, total * 8, cudaMemcpyDeviceToHost, s));
-    }
+    CU_CHECK(cudaMemcpyAsync(w.pin_ids, w.out_ids, total * 4, cudaMemcpyDeviceToHost, s));
+    if (want_round) CU_CHECK(cudaMemcpyAsync(w.pin_round, w.out_round, total * 2, cudaMemcpyDeviceToHost, s));
+    if (need_w) CU_CHECK(cudaMemcpyAsync(w.pin_w, w.out_w, total * 8, cudaMemcpyDeviceToHost, s));
+    if (int_sum) CU_CHECK(cudaMemcpyAsync(&isum, w.int_sum, 8, cudaMemcpyDeviceToHost, s));
   }
   if (rounds) {
     CU_CHECK(cudaMemcpyAsync(out->per_round_matched, w.matched_cnt + 1, rounds * 4ull, cudaMemcpyDeviceToHost, s));
@@ -725,10 +763,17 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   float ms = 0.f;
   CU_CHECK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   out->device_ms = ms;
+  if (total) {
+    std::memcpy(out->matched_edges, w.pin_ids, total * 4);
+    if (want_round) std::memcpy(out->matched_round, w.pin_round, total * 2);
+  }
   // total_weight accumulates base weights in ascending-id order (local_max_seq.hpp:79)
   double tw = 0.0;
   if (need_w) {
+    const double* wts = static_cast<const double*>(w.pin_w);
     for (uint64_t i = 0; i < total; ++i) tw += wts[i];
+  } else if (int_sum) {
+    tw = static_cast<double>(isum);
   } else {
     const double b = g->base_const;
     if (b == std::floor(b) && b * static_cast<double>(total) < 9007199254740992.0) {

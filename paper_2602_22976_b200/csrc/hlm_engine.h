@@ -16,7 +16,12 @@ struct Workspace {
   unsigned long long* vkey = nullptr;
   uint32_t* dead = nullptr;
   uint16_t* mround = nullptr;
-  uint32_t* list[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint32_t* mbits = nullptr;
+  uint32_t mbits_words = 0;
+  uint32_t* seg_ids[2] = {nullptr, nullptr};
+  uint32_t* seg_cnt[2] = {nullptr, nullptr};
+  uint32_t nseg = 0, seg_cap = 0;
+  uint32_t* list1[2] = {nullptr, nullptr};
   uint8_t* mflag[2] = {nullptr, nullptr};
   uint32_t* matched_cnt = nullptr;
   uint32_t* deact_cnt = nullptr;
@@ -33,6 +38,12 @@ struct Workspace {
   uint16_t* out_round = nullptr;
   double* out_w = nullptr;
   uint64_t out_cap = 0;
+  unsigned long long* int_sum = nullptr;
+  // pinned host staging for the device-to-host copy of the result
+  void* pin_ids = nullptr;
+  void* pin_round = nullptr;
+  void* pin_w = nullptr;
+  uint64_t pin_cap = 0;
   // CUDA-graph WHILE loop over the round body
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -63,6 +74,7 @@ struct Graph {
   double* base = nullptr;  // null: all weights equal base_const
   double base_const = 1.0;
   double base_min = 1.0, base_max = 1.0;
+  bool base_integral = true;  // every base weight is an integer below 2^32 (order-free exact sums)
   // vertex -> incident edges, built on the device when a variant (crew) or a download needs it
   uint64_t* voff = nullptr;  // n+1
   uint32_t* vinc = nullptr;  // kappa

@@ -7,73 +7,143 @@
 namespace hlmb {
 
 // ---------------------------------------------------------------------------------------------
-// Round kernels, class 0: one thread per edge (size <= kLargeEdge).  D > 0: uniform edge size
-// with one 64/128-bit pin load per thread; D == 0: runtime offsets.
+// Round kernels, class 0: one thread per edge (size <= kLargeEdge), ITEMS edges per thread and
+// tile.  D > 0: uniform edge size, one 64/128-bit pin load per edge; D == 0: runtime offsets.
 // ---------------------------------------------------------------------------------------------
+template <int D>
+struct TileShape {
+  static constexpr int kItems = D == 2 ? 4 : (D == 4 ? 2 : 1);
+  static constexpr uint32_t kTile = kBlock * kItems;
+};
+
+__device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
+                                                 uint32_t seg) {
+  if (!ident) return cnt[seg];
+  const uint64_t b = static_cast<uint64_t>(seg) * P.seg_cap;
+  return b >= P.m ? 0u : static_cast<uint32_t>(min(static_cast<uint64_t>(P.seg_cap), P.m - b));
+}
+
 template <int D, bool VMAX>
 __global__ void __launch_bounds__(kBlock) k_filter_vmax_small(const RoundParams P) {
-  __shared__ uint32_t s_warp[kWarpsPerBlock];
-  __shared__ uint32_t s_base;
+  constexpr int ITEMS = TileShape<D>::kItems;
+  constexpr uint32_t TILE = TileShape<D>::kTile;
+  __shared__ uint32_t s_cnt[ITEMS * kWarpsPerBlock];
+  __shared__ uint32_t s_seg;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
-  const uint32_t cnt = c->count[par][0];
-  const bool in_ident = P.ident0 && r <= 2;
-  const bool out_ident = P.ident0 && r == 1;
-  const uint32_t* __restrict__ in = P.list[0][par];
-  uint32_t* __restrict__ out = P.list[0][par ^ 1];
-  const uint8_t* __restrict__ mflag = P.mflag[0];
+  const bool in_ident = r <= 2;   // rounds 1 and 2 read the identity list
+  const bool out_ident = r == 1;  // round 1 keeps every edge: nothing to write
+  const uint32_t* __restrict__ in = P.seg_ids[par];
+  const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
+  uint32_t* __restrict__ out = P.seg_ids[par ^ 1];
+  uint32_t* __restrict__ out_cnt = P.seg_cnt[par ^ 1];
+  const uint8_t* __restrict__ mflag = P.mflag0;
   const uint32_t tag = round_tag(P.ks, r);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t local_deact = 0;
   bool tie = false;
 
-  if (out_ident && blockIdx.x == 0 && threadIdx.x == 0) c->count[par ^ 1][0] = cnt;
-
-  const uint32_t tiles = (cnt + kBlock - 1) / kBlock;
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const uint32_t pos = tile * kBlock + threadIdx.x;
-    bool survive = false;
-    uint32_t e = 0;
-    if (pos < cnt) {
-      e = in_ident ? pos : in[pos];
-      const bool was_matched = r > 1 && mflag[pos];
-      if (!was_matched) {
-        if constexpr (D > 0) {
-          const PinVec<D> pv = load_pins<D>(P.csr.pins, e);
-          bool dead_any = false;
-          if (r > 1) {
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_seg = atomicAdd(&c->ticket_f, 1u);
+    __syncthreads();
+    const uint32_t seg = s_seg;
+    if (seg >= P.nseg) break;
+    const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
+    const uint32_t seg_base = seg * P.seg_cap;
+    uint32_t out_off = 0;
+    for (uint32_t t0 = 0; t0 < cnt; t0 += TILE) {
+      uint32_t e[ITEMS];
+      bool survive[ITEMS];
 #pragma unroll
-            for (int i = 0; i < D; ++i) dead_any |= vertex_dead(P.dead, pv.v[i]);
-          }
-          if (dead_any) {
-            ++local_deact;
-          } else {
-            survive = true;
-            if constexpr (VMAX) {
-              const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
-              unsigned long long old[D];
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t idx = t0 + k * kBlock + threadIdx.x;
+        survive[k] = false;
+        e[k] = 0;
+        if (idx < cnt) {
+          const uint32_t phys = seg_base + idx;
+          e[k] = in_ident ? phys : in[phys];
+          survive[k] = !(r > 1 && mflag[phys]);
+        }
+      }
+      if constexpr (D > 0) {
+        PinVec<D> pv[ITEMS];
 #pragma unroll
-              for (int i = 0; i < D; ++i) old[i] = atomicMax(P.vkey + pv.v[i], key);
+        for (int k = 0; k < ITEMS; ++k)
+          if (survive[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
+        if (r > 1) {
 #pragma unroll
-              for (int i = 0; i < D; ++i) tie |= (old[i] == key);
+          for (int k = 0; k < ITEMS; ++k) {
+            if (!survive[k]) continue;
+            bool dead_any = false;
+#pragma unroll
+            for (int i = 0; i < D; ++i) dead_any |= vertex_dead(P.dead, pv[k].v[i]);
+            if (dead_any) {
+              survive[k] = false;
+              ++local_deact;
             }
           }
-        } else {
+        }
+        if constexpr (VMAX) {
+          unsigned long long key[ITEMS];
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k)
+            if (survive[k])
+              key[k] = priority_key(P.stream, P.ks, e[k] + P.id_base, r, base_of(P, e[k]), tag);
+          if (P.ks.precheck) {
+            unsigned long long cur[ITEMS][D];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+              if (survive[k]) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) cur[k][i] = __ldcg(P.vkey + pv[k].v[i]);
+              }
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+              if (survive[k]) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                  if (cur[k][i] < key[k])
+                    tie |= (atomicMax(P.vkey + pv[k].v[i], key[k]) == key[k]);
+                  else
+                    tie |= (cur[k][i] == key[k]);
+                }
+              }
+          } else {
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+              if (survive[k]) {
+                unsigned long long old[D];
+#pragma unroll
+                for (int i = 0; i < D; ++i) old[i] = atomicMax(P.vkey + pv[k].v[i], key[k]);
+#pragma unroll
+                for (int i = 0; i < D; ++i) tie |= (old[i] == key[k]);
+              }
+          }
+        }
+      } else {
+        // runtime sizes: ITEMS == 1
+        if (survive[0]) {
           uint64_t b;
           uint32_t s;
-          P.csr.range(e, b, s);
-          if (!(P.has_large && s > kLargeEdge)) {  // large edges belong to class 1
+          P.csr.range(e[0], b, s);
+          if (P.has_large && s > kLargeEdge) {
+            survive[0] = false;  // class-1 edge seen through the identity list
+          } else {
             const uint32_t* __restrict__ pp = P.csr.pins + b;
             bool dead_any = false;
             if (r > 1)
               for (uint32_t i = 0; i < s; ++i) dead_any |= vertex_dead(P.dead, __ldg(pp + i));
             if (dead_any) {
+              survive[0] = false;
               ++local_deact;
-            } else {
-              survive = true;
-              if constexpr (VMAX) {
-                const unsigned long long key =
-                    priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
+            } else if constexpr (VMAX) {
+              const unsigned long long key =
+                  priority_key(P.stream, P.ks, e[0] + P.id_base, r, base_of(P, e[0]), tag);
+              if (P.ks.precheck) {
+                for (uint32_t i = 0; i < s; ++i) tie |= vertex_max(P.vkey + __ldg(pp + i), key);
+              } else {
                 for (uint32_t i = 0; i < s; ++i)
                   tie |= (atomicMax(P.vkey + __ldg(pp + i), key) == key);
               }
@@ -81,71 +151,140 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_small(const RoundParams 
           }
         }
       }
+      if (!out_ident) {
+        // order-preserving compaction of the tile: (item, warp) counts, then a short serial scan
+        uint32_t within[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t ballot = __ballot_sync(0xffffffffu, survive[k]);
+          within[k] = __popc(ballot & ((1u << lane) - 1u));
+          if (lane == 0) s_cnt[k * kWarpsPerBlock + warp] = __popc(ballot);
+        }
+        __syncthreads();
+        uint32_t run = 0, mine[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+#pragma unroll
+          for (int w = 0; w < kWarpsPerBlock; ++w) {
+            if (w == static_cast<int>(warp)) mine[k] = run;
+            run += s_cnt[k * kWarpsPerBlock + w];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (survive[k]) out[seg_base + out_off + mine[k] + within[k]] = e[k];
+        out_off += run;
+        __syncthreads();
+      }
     }
-    if (!out_ident) {
-      uint32_t total;
-      const uint32_t rank = block_rank(survive, s_warp, total);
-      if (threadIdx.x == 0) s_base = total ? atomicAdd(&c->count[par ^ 1][0], total) : 0u;
-      __syncthreads();
-      if (survive) out[s_base + rank] = e;
+    if (threadIdx.x == 0) {
+      const uint32_t kept = out_ident ? cnt : out_off;
+      out_cnt[seg] = kept;
+      if (kept) atomicAdd(&c->active_small, kept);
     }
   }
-  const uint32_t d = block_sum(local_deact, s_warp);
+  const uint32_t d = block_sum(local_deact, s_cnt);
   if (threadIdx.x == 0 && d) atomicAdd(P.deact_cnt + (r - 1), d);
   if (tie) c->tie_flag = 1u;
 }
 
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_check_commit_small(const RoundParams P) {
+  constexpr int ITEMS = TileShape<D>::kItems;
+  constexpr uint32_t TILE = TileShape<D>::kTile;
   __shared__ uint32_t s_warp[kWarpsPerBlock];
-  const Ctrl* c = P.ctrl;
+  __shared__ uint32_t s_seg;
+  Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
   const uint32_t par = c->parity;
-  const uint32_t cnt = c->count[par ^ 1][0];
-  const bool ident = P.ident0 && r == 1;
-  const uint32_t* __restrict__ list = P.list[0][par ^ 1];
-  uint8_t* __restrict__ mflag = P.mflag[0];
+  const bool ident = r == 1;
+  const uint32_t* __restrict__ list = P.seg_ids[par ^ 1];
+  const uint32_t* __restrict__ list_cnt = P.seg_cnt[par ^ 1];
+  uint8_t* __restrict__ mflag = P.mflag0;
   const uint32_t tag = round_tag(P.ks, r);
   uint32_t local_matched = 0;
 
-  for (uint32_t pos = blockIdx.x * kBlock + threadIdx.x; pos < cnt; pos += gridDim.x * kBlock) {
-    const uint32_t e = ident ? pos : list[pos];
-    bool win = true;
-    if constexpr (D > 0) {
-      const PinVec<D> pv = load_pins<D>(P.csr.pins, e);
-      const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
-      unsigned long long top[D];
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_seg = atomicAdd(&c->ticket_c, 1u);
+    __syncthreads();
+    const uint32_t seg = s_seg;
+    if (seg >= P.nseg) break;
+    const uint32_t cnt = list_cnt[seg];
+    const uint32_t seg_base = seg * P.seg_cap;
+    for (uint32_t t0 = 0; t0 < cnt; t0 += TILE) {
+      uint32_t e[ITEMS];
+      bool valid[ITEMS], win[ITEMS];
 #pragma unroll
-      for (int i = 0; i < D; ++i) top[i] = __ldg(P.vkey + pv.v[i]);
-#pragma unroll
-      for (int i = 0; i < D; ++i) win &= (top[i] == key);
-      if (win) {
-        P.mround[e] = static_cast<uint16_t>(r);
-#pragma unroll
-        for (int i = 0; i < D; ++i) atomicOr(P.dead + (pv.v[i] >> 5), 1u << (pv.v[i] & 31));
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t idx = t0 + k * kBlock + threadIdx.x;
+        valid[k] = idx < cnt;
+        win[k] = false;
+        e[k] = valid[k] ? (ident ? seg_base + idx : list[seg_base + idx]) : 0u;
       }
-    } else {
-      uint64_t b;
-      uint32_t s;
-      P.csr.range(e, b, s);
-      if (P.has_large && s > kLargeEdge) {
-        win = false;  // not this class's edge (identity list only)
+      if constexpr (D > 0) {
+        PinVec<D> pv[ITEMS];
+        unsigned long long key[ITEMS], top[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (valid[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
+        // first pin of every item in flight together; most edges lose right here
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (valid[k]) top[k] = __ldg(P.vkey + pv[k].v[0]);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (valid[k]) {
+            key[k] = priority_key(P.stream, P.ks, e[k] + P.id_base, r, base_of(P, e[k]), tag);
+            win[k] = top[k] == key[k];
+          }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (win[k]) {
+            unsigned long long rest[D];
+#pragma unroll
+            for (int i = 1; i < D; ++i) rest[i] = __ldg(P.vkey + pv[k].v[i]);
+#pragma unroll
+            for (int i = 1; i < D; ++i) win[k] &= (rest[i] == key[k]);
+          }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (win[k]) {
+            P.mround[e[k]] = static_cast<uint16_t>(r);
+            atomicOr(P.mbits + (e[k] >> 5), 1u << (e[k] & 31));
+#pragma unroll
+            for (int i = 0; i < D; ++i) atomicOr(P.dead + (pv[k].v[i] >> 5), 1u << (pv[k].v[i] & 31));
+            ++local_matched;
+          }
       } else {
-        const uint32_t* __restrict__ pp = P.csr.pins + b;
-        const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
-        for (uint32_t i = 0; i < s && win; ++i) win = (__ldg(P.vkey + __ldg(pp + i)) == key);
-        if (win) {
-          P.mround[e] = static_cast<uint16_t>(r);
-          for (uint32_t i = 0; i < s; ++i) {
-            const uint32_t v = __ldg(pp + i);
-            atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+        if (valid[0]) {
+          uint64_t b;
+          uint32_t s;
+          P.csr.range(e[0], b, s);
+          if (!(P.has_large && s > kLargeEdge)) {
+            const uint32_t* __restrict__ pp = P.csr.pins + b;
+            const unsigned long long key =
+                priority_key(P.stream, P.ks, e[0] + P.id_base, r, base_of(P, e[0]), tag);
+            bool w = true;
+            for (uint32_t i = 0; i < s && w; ++i) w = (__ldg(P.vkey + __ldg(pp + i)) == key);
+            if (w) {
+              P.mround[e[0]] = static_cast<uint16_t>(r);
+              atomicOr(P.mbits + (e[0] >> 5), 1u << (e[0] & 31));
+              for (uint32_t i = 0; i < s; ++i) {
+                const uint32_t v = __ldg(pp + i);
+                atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+              }
+              ++local_matched;
+            }
+            win[0] = w;
           }
         }
       }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (valid[k]) mflag[seg_base + t0 + k * kBlock + threadIdx.x] = win[k] ? 1 : 0;
     }
-    mflag[pos] = win ? 1 : 0;
-    local_matched += win ? 1u : 0u;
   }
   const uint32_t t = block_sum(local_matched, s_warp);
   if (threadIdx.x == 0 && t) atomicAdd(P.matched_cnt + r, t);
@@ -159,10 +298,10 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
-  const uint32_t cnt = c->count[par][1];
-  const uint32_t* __restrict__ in = P.list[1][par];
-  uint32_t* __restrict__ out = P.list[1][par ^ 1];
-  const uint8_t* __restrict__ mflag = P.mflag[1];
+  const uint32_t cnt = c->count1[par];
+  const uint32_t* __restrict__ in = P.list1[par];
+  uint32_t* __restrict__ out = P.list1[par ^ 1];
+  const uint8_t* __restrict__ mflag = P.mflag1;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -184,10 +323,10 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
       local_deact += (lane == 0);
       continue;
     }
-    if (lane == 0) out[atomicAdd(&c->count[par ^ 1][1], 1u)] = e;
+    if (lane == 0) out[atomicAdd(&c->count1[par ^ 1], 1u)] = e;
     if constexpr (VMAX) {
       const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
-      for (uint32_t i = lane; i < s; i += 32) tie |= (atomicMax(P.vkey + __ldg(pp + i), key) == key);
+      for (uint32_t i = lane; i < s; i += 32) tie |= vertex_max(P.vkey + __ldg(pp + i), key);
     }
   }
   if (local_deact) atomicAdd(P.deact_cnt + (r - 1), local_deact);
@@ -199,9 +338,9 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
   const uint32_t par = c->parity;
-  const uint32_t cnt = c->count[par ^ 1][1];
-  const uint32_t* __restrict__ list = P.list[1][par ^ 1];
-  uint8_t* __restrict__ mflag = P.mflag[1];
+  const uint32_t cnt = c->count1[par ^ 1];
+  const uint32_t* __restrict__ list = P.list1[par ^ 1];
+  uint8_t* __restrict__ mflag = P.mflag1;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -228,6 +367,7 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
       }
       if (lane == 0) {
         P.mround[e] = static_cast<uint16_t>(r);
+        atomicOr(P.mbits + (e >> 5), 1u << (e & 31));
         ++local_matched;
       }
     }
@@ -241,8 +381,10 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
 __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle, int in_graph) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round, par = c->parity;
-  const uint32_t active = c->count[par ^ 1][0] + c->count[par ^ 1][1];
+  const uint32_t active = c->active_small + c->count1[par ^ 1];
   uint32_t status = ST_RUNNING;
+  c->ticket_f = 0;
+  c->ticket_c = 0;
   if (c->tie_flag) {
     status = ST_TIE;
   } else if (active == 0) {
@@ -253,9 +395,9 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
     c->rounds_done = r - 1;
   } else {
     c->edges_swept += active;
+    c->active_small = 0;
     c->parity = par ^ 1;
-    c->count[par][0] = 0;
-    c->count[par][1] = 0;
+    c->count1[par] = 0;
     c->round = r + 1;
     if (r % P.ks.tag_period == 0) status = ST_EPOCH;
   }
@@ -270,33 +412,43 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
 struct ExactParams {
   unsigned long long* va;  // n: max weight bits
   unsigned long long* vb;  // n: max tie hash among weight maxima
-  uint32_t* vc;            // n: max (id + 1) among (weight, hash) maxima
-  const uint32_t* list;    // null: identity
-  uint32_t count;
+  uint32_t* vc;            // n: max (global id + 1) among (weight, hash) maxima
   uint32_t round;
-  uint32_t cls;            // 0: skip large edges of an identity list; 1: list of large edges
-  uint8_t* mflag;
+  uint32_t cls;            // 0: segmented lists of buffer `buf`; 1: appended list of large edges
+  uint32_t buf;
+  uint32_t ident;          // class 0 only: the list is the identity
+  uint32_t count1;         // class 1 length
 };
 
 template <int LEVEL>
 __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, const ExactParams X) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
+  const uint64_t warp = blockIdx.x * static_cast<uint64_t>(kWarpsPerBlock) + (threadIdx.x >> 5);
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
   const uint32_t r = X.round;
+  const uint64_t slots = X.cls == 0 ? static_cast<uint64_t>(P.nseg) * P.seg_cap : X.count1;
+  uint8_t* mflag = X.cls == 0 ? P.mflag0 : P.mflag1;
   uint32_t local_matched = 0;
-  for (uint32_t pos = warp; pos < X.count; pos += nwarps) {
-    const uint32_t e = X.list ? X.list[pos] : pos;
+  for (uint64_t pos = warp; pos < slots; pos += nwarps) {
+    uint32_t e;
+    if (X.cls == 0) {
+      const uint32_t seg = static_cast<uint32_t>(pos / P.seg_cap);
+      const uint32_t idx = static_cast<uint32_t>(pos % P.seg_cap);
+      if (idx >= region_count(P, X.ident, P.seg_cnt[X.buf], seg)) continue;
+      e = X.ident ? static_cast<uint32_t>(pos) : P.seg_ids[X.buf][pos];
+    } else {
+      e = P.list1[X.buf][pos];
+    }
     uint64_t b;
     uint32_t s;
     P.csr.range(e, b, s);
     if (X.cls == 0 && P.has_large && s > kLargeEdge) {
-      if (LEVEL == 4 && lane == 0) X.mflag[pos] = 0;
+      if (LEVEL == 4 && lane == 0) mflag[pos] = 0;
       continue;
     }
     const uint32_t* __restrict__ pp = P.csr.pins + b;
-    const unsigned long long A =
-        static_cast<unsigned long long>(__double_as_longlong(edge_weight(P.stream, e + P.id_base, r, base_of(P, e))));
+    const unsigned long long A = static_cast<unsigned long long>(
+        __double_as_longlong(edge_weight(P.stream, e + P.id_base, r, base_of(P, e))));
     const unsigned long long B = tie_hash(P.stream, e + P.id_base, r);
     const uint32_t C = e + P.id_base + 1u;
     bool win = true;
@@ -321,10 +473,11 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
         }
         if (lane == 0) {
           P.mround[e] = static_cast<uint16_t>(r);
+          atomicOr(P.mbits + (e >> 5), 1u << (e & 31));
           ++local_matched;
         }
       }
-      if (lane == 0) X.mflag[pos] = win ? 1 : 0;
+      if (lane == 0) mflag[pos] = win ? 1 : 0;
     }
   }
   if (LEVEL == 4 && local_matched) atomicAdd(P.matched_cnt + r, local_matched);
@@ -431,21 +584,20 @@ __global__ void k_eval_stream(const StreamParams s, const uint32_t* edges, const
 }
 
 // ---------------------------------------------------------------------------------------------
-// Result assembly (finish_matching, local_max_seq.hpp:74-83): ordered compaction of mround[].
+// Result assembly (finish_matching, local_max_seq.hpp:74-83): ordered compaction of the matched
+// bitmap; ids come out ascending, with the round and (optionally) the base weight of each.
 // ---------------------------------------------------------------------------------------------
-constexpr int kAsmItems = 16;  // entries per thread
-constexpr uint32_t kAsmChunk = kBlock * kAsmItems;
+constexpr int kAsmWords = 8;  // bitmap words per thread
+constexpr uint32_t kAsmChunkWords = kBlock * kAsmWords;
 
-__global__ void __launch_bounds__(kBlock) k_assemble_count(const uint16_t* mround, uint32_t m,
+__global__ void __launch_bounds__(kBlock) k_assemble_count(const uint32_t* mbits, uint32_t words,
                                                            uint32_t* chunk_cnt) {
   __shared__ uint32_t s_warp[kWarpsPerBlock];
-  const uint32_t base = blockIdx.x * kAsmChunk;
+  const uint32_t w0 = blockIdx.x * kAsmChunkWords + threadIdx.x * kAsmWords;
   uint32_t c = 0;
 #pragma unroll
-  for (int k = 0; k < kAsmItems; ++k) {
-    const uint32_t e = base + k * kBlock + threadIdx.x;
-    if (e < m) c += mround[e] != 0;
-  }
+  for (int k = 0; k < kAsmWords; ++k)
+    if (w0 + k < words) c += __popc(mbits[w0 + k]);
   const uint32_t t = block_sum(c, s_warp);
   if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = t;
 }
@@ -455,23 +607,21 @@ __global__ void __launch_bounds__(1024) k_scan_small(uint32_t* vals, uint32_t cn
                                                      unsigned long long* total) {
   __shared__ unsigned long long s_part[1024];
   const uint32_t per = (cnt + 1023) / 1024;
-  const uint32_t b = threadIdx.x * per;
+  const uint32_t b = min(cnt, threadIdx.x * per);
   const uint32_t e = min(cnt, b + per);
   unsigned long long acc = 0;
   for (uint32_t i = b; i < e; ++i) acc += vals[i];
+  // inclusive scan of the 1024 partials (Hillis-Steele in shared memory)
   s_part[threadIdx.x] = acc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long run = 0;
-    for (int i = 0; i < 1024; ++i) {
-      const unsigned long long v = s_part[i];
-      s_part[i] = run;
-      run += v;
-    }
-    *total = run;
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned long long t = threadIdx.x >= static_cast<unsigned>(o) ? s_part[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    s_part[threadIdx.x] += t;
+    __syncthreads();
   }
-  __syncthreads();
-  unsigned long long run = s_part[threadIdx.x];
+  if (threadIdx.x == 1023) *total = s_part[1023];
+  unsigned long long run = s_part[threadIdx.x] - acc;
   for (uint32_t i = b; i < e; ++i) {
     const uint32_t v = vals[i];
     vals[i] = static_cast<uint32_t>(run);
@@ -479,28 +629,49 @@ __global__ void __launch_bounds__(1024) k_scan_small(uint32_t* vals, uint32_t cn
   }
 }
 
-__global__ void __launch_bounds__(kBlock) k_assemble_write(const uint16_t* mround, uint32_t m,
+__global__ void __launch_bounds__(kBlock) k_assemble_write(const uint32_t* mbits, uint32_t words,
                                                            const uint32_t* chunk_off,
-                                                           const double* base, uint32_t id_base,
-                                                           uint32_t* out_ids,
-                                                           uint16_t* out_round, double* out_w) {
+                                                           const uint16_t* mround, const double* base,
+                                                           uint32_t id_base, uint32_t* out_ids,
+                                                           uint16_t* out_round, double* out_w,
+                                                           unsigned long long* int_weight_sum) {
   __shared__ uint32_t s_warp[kWarpsPerBlock];
-  const uint32_t base_e = blockIdx.x * kAsmChunk;
-  uint32_t running = chunk_off[blockIdx.x];
-  // entries are visited in id order: item k covers a contiguous run of kBlock ids
-  for (int k = 0; k < kAsmItems; ++k) {
-    const uint32_t e = base_e + k * kBlock + threadIdx.x;
-    const uint16_t r = e < m ? mround[e] : 0;
-    uint32_t total;
-    const uint32_t rank = block_rank(r != 0, s_warp, total);
-    if (r != 0) {
-      const uint32_t o = running + rank;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t w0 = blockIdx.x * kAsmChunkWords + threadIdx.x * kAsmWords;
+  uint32_t bits[kAsmWords];
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < kAsmWords; ++k) {
+    bits[k] = w0 + k < words ? mbits[w0 + k] : 0u;
+    c += __popc(bits[k]);
+  }
+  uint32_t incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t o = chunk_off[blockIdx.x] + incl - c;
+  for (uint32_t w = 0; w < warp; ++w) o += s_warp[w];
+  unsigned long long wsum = 0;
+#pragma unroll
+  for (int k = 0; k < kAsmWords; ++k) {
+    uint32_t b = bits[k];
+    while (b) {
+      const uint32_t bit = __ffs(b) - 1;
+      b &= b - 1;
+      const uint32_t e = (w0 + k) * 32u + bit;
       out_ids[o] = e + id_base;
-      if (out_round) out_round[o] = r;
+      if (out_round) out_round[o] = mround[e];
       if (out_w) out_w[o] = base[e];
+      if (int_weight_sum) wsum += static_cast<unsigned long long>(base[e]);
+      ++o;
     }
-    running += total;
-    __syncthreads();
+  }
+  if (int_weight_sum) {
+    for (int s = 16; s > 0; s >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, s);
+    if (lane == 0 && wsum) atomicAdd(int_weight_sum, wsum);
   }
 }
 

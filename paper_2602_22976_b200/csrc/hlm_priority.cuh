@@ -37,6 +37,7 @@ struct KeyScheme {
   int32_t payload_bits;  // 1..63
   int32_t hash_bits;     // KEY_INT_HASH only
   uint32_t tag_period;   // number of distinct non-zero tags = 2^(64-payload_bits) - 1 (capped)
+  uint32_t precheck;     // filter atomics with a plain L2 load of the running maximum first
   uint64_t wmin_bits;    // KEY_WEIGHT_BITS: bits of the smallest possible weight
   uint64_t wq_min;       // KEY_INT_HASH: smallest integer weight
 };

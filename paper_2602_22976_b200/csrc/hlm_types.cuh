@@ -1,19 +1,24 @@
-// hlm_types.cuh -- shared device types / helpers for the sm_100a kernels of the local-max matching round (CRCW variant) plus the
-// loader / result-assembly helpers.  Reference semantics: local_max_par.hpp:93-253
-// (run_soft_delete + local_max_crcw) and local_max_seq.hpp:22-90; see DESIGN.md for the mapping
-// of reference phases onto these kernels.
+// hlm_types.cuh -- device-side types and helpers shared by the translation units of
+// libhlm_b200.so.  Reference semantics: local_max_par.hpp:93-253 (run_soft_delete +
+// local_max_crcw) and local_max_seq.hpp:22-90; DESIGN.md maps reference phases onto kernels.
 //
-// Round r on the device (one "step" of the WHILE graph):
+// Round r on the device (one iteration of the CUDA-graph WHILE body):
 //   k_filter_vmax  -- for every edge that was active in round r-1: drop it if it matched, drop it
-//                     (and count it as deactivated) if one of its pins died, otherwise append it to
-//                     the round-r active list and atomicMax its round-tagged key into vkey[pin].
-//                     (reference phases: deactivation :229-248, collect :163, weight refresh
-//                     :126-135 and vertex argmax :137-159, fused)
+//                     (counted as deactivated) if one of its pins died, otherwise keep it in the
+//                     round-r active list and atomicMax its round-tagged key into vkey[pin].
+//                     (reference: deactivation :229-248, collect :163, weight refresh :126-135,
+//                     vertex argmax :137-159 -- fused into one pass over the pins)
 //   k_check_commit -- an active edge is matched iff its key is the maximum at every pin
-//                     (== agreement count :202-224); matched edges record their round and set the
-//                     dead bit of their pins (completion marking :221).
+//                     (== agreement count == |e|, :202-224); matched edges record their round
+//                     and set the dead bit of their pins (completion marking :221).
 //   k_advance      -- one thread: round bookkeeping, termination, round cap, tie / epoch exits.
-// All memory-bound integer work: no tensor cores.
+// All of it is memory-bound integer work: no tensor cores.
+//
+// Active lists (class 0 = edges with <= 32 pins, one thread per edge) are SEGMENTED: the edge-id
+// space is cut into nseg regions of seg_cap ids; a CTA claims a region by ticket, filters it and
+// writes the survivors back into the same region of the other buffer.  No global scan, no
+// contended append counter, and the lists stay in ascending-id order (deterministic content,
+// monotone pin addresses).  Class 1 (larger edges, one warp per edge) is a plain appended list.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -34,16 +39,19 @@ enum LoopStatus : uint32_t {
   ST_EPOCH = 4,  // round tags wrapped: vkey must be cleared before continuing
 };
 
-// Device-resident loop state; every kernel reads it, k_advance is its only writer besides the
-// per-list counters.
+// Device-resident loop state.
 struct Ctrl {
   uint32_t round;        // round being processed (1-based)
-  uint32_t parity;       // list buffer holding the previous round's active list
-  uint32_t count[2][2];  // [buffer][class] list lengths
+  uint32_t parity;       // list buffer holding the previous round's active lists
+  uint32_t ticket_f;     // region tickets of the filter kernel
+  uint32_t ticket_c;     // region tickets of the check kernel
+  uint32_t active_small; // class-0 edges active in this round (sum of region counts)
+  uint32_t count1[2];    // [buffer] class-1 list lengths
   uint32_t tie_flag;
   uint32_t status;
   uint32_t max_rounds;
   uint32_t rounds_done;
+  uint32_t pad;
   unsigned long long edges_swept;  // sum over rounds of the active-list lengths
 };
 
@@ -75,16 +83,23 @@ struct RoundParams {
   uint32_t n;
   uint32_t m;
   uint32_t has_large;  // some edges have more than kLargeEdge pins
-  uint32_t id_base;    // global id of local edge 0 (edge-partitioned instances); priorities use global ids
+  uint32_t id_base;    // global id of local edge 0 (edge shards); priorities use global ids
   StreamParams stream;
   KeyScheme ks;
   Ctrl* ctrl;
   unsigned long long* vkey;  // n round-tagged vertex maxima
   uint32_t* dead;            // n bits: vertex covered by a matched edge
-  uint16_t* mround;          // m: 0 = not matched, else the round it matched in
-  uint32_t* list[2][2];      // [class][buffer] active-edge lists
-  uint8_t* mflag[2];         // [class] per list position: matched in the round just checked
-  uint32_t ident0;           // class-0 list of round 1 is the identity (no array)
+  uint32_t* mbits;           // m bits: edge matched
+  uint16_t* mround;          // m: round an edge matched in (valid where its mbits bit is set)
+  // class 0: segmented lists
+  uint32_t* seg_ids[2];      // [buffer] nseg regions of seg_cap edge ids
+  uint32_t* seg_cnt[2];      // [buffer][nseg] ids in use per region
+  uint32_t nseg;
+  uint32_t seg_cap;
+  uint8_t* mflag0;           // per class-0 list slot: matched in the round just checked
+  // class 1: appended list
+  uint32_t* list1[2];
+  uint8_t* mflag1;
   uint32_t* matched_cnt;     // [round] edges matched in that round
   uint32_t* deact_cnt;       // [round] edges deactivated in that round
 };
@@ -122,6 +137,7 @@ __device__ __forceinline__ PinVec<8> load_pins<8>(const uint32_t* pins, uint32_t
 }
 
 // Block-wide exclusive offset of `flag` plus the block total (warp ballot + scan of 8 warp sums).
+// Callers must __syncthreads() before the next use of s_warp.
 __device__ __forceinline__ uint32_t block_rank(bool flag, uint32_t* s_warp, uint32_t& total) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t ballot = __ballot_sync(0xffffffffu, flag);
@@ -148,6 +164,17 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, uint32_t* s_warp) {
 #pragma unroll
   for (int w = 0; w < kWarpsPerBlock; ++w) s += s_warp[w];
   return s;
+}
+
+// vkey[v] = max(vkey[v], key) with tie detection.  A plain L2 load filters out edges that
+// already lost (the running maximum only grows), so only O(log deg) of a vertex's edges reach
+// the atomic unit.  Returns true if another edge deposited the same key (this
+// detection is complete for the key that ends up being the maximum).
+__device__ __forceinline__ bool vertex_max(unsigned long long* slot, unsigned long long key) {
+  const unsigned long long cur = __ldcg(slot);
+  if (cur > key) return false;
+  if (cur == key) return true;
+  return atomicMax(slot, key) == key;
 }
 
 struct WeightStats {
