@@ -333,12 +333,13 @@ static int ensure_workspace(Graph* g, uint32_t max_rounds) {
     ST_CHECK(dev_alloc(&w.mround, g->m, g));
     w.mbits_words = (g->m + 31) / 32;
     ST_CHECK(dev_alloc(&w.mbits, w.mbits_words, g));
-    // class-0 lists: regions of seg_cap edge ids, several regions per resident CTA so that the
-    // ticket scheduler can balance uneven survivor counts
-    const uint32_t target = static_cast<uint32_t>(g->num_sms) * 64u;
-    w.seg_cap = std::max<uint32_t>(1024u, (g->m + target - 1) / std::max(1u, target));
-    w.seg_cap = (w.seg_cap + 1023u) / 1024u * 1024u;
+    // class-0 lists: one region of seg_cap edge ids per warp, a CTA claims 8 regions at a time;
+    // several claims per resident CTA so the ticket scheduler can balance uneven survivor counts
+    const uint32_t target = static_cast<uint32_t>(g->num_sms) * 64u * kWarpsPerBlock;
+    w.seg_cap = std::max<uint32_t>(128u, (g->m + target - 1) / std::max(1u, target));
+    w.seg_cap = (w.seg_cap + 63u) / 64u * 64u;
     w.nseg = std::max<uint32_t>(1u, (g->m + w.seg_cap - 1) / w.seg_cap);
+    w.nseg = (w.nseg + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
     for (int b = 0; b < 2; ++b) {
       ST_CHECK(dev_alloc(&w.seg_ids[b], static_cast<size_t>(w.nseg) * w.seg_cap, g));
       ST_CHECK(dev_alloc(&w.seg_cnt[b], w.nseg, g));

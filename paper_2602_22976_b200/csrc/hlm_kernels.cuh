@@ -12,8 +12,8 @@ namespace hlmb {
 // ---------------------------------------------------------------------------------------------
 template <int D>
 struct TileShape {
-  static constexpr int kItems = D == 2 ? 4 : (D == 4 ? 2 : 1);
-  static constexpr uint32_t kTile = kBlock * kItems;
+  static constexpr int kItems = (D == 2 || D == 4) ? 2 : 1;  // edges per lane and step
+  static constexpr uint32_t kStep = 32 * kItems;             // edges per warp and step
 };
 
 __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
@@ -23,12 +23,14 @@ __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool iden
   return b >= P.m ? 0u : static_cast<uint32_t>(min(static_cast<uint64_t>(P.seg_cap), P.m - b));
 }
 
+// A CTA claims kWarpsPerBlock consecutive regions by ticket; each warp then owns one region and
+// runs on its own (ballot / popc compaction, no block barrier inside the sweep).
 template <int D, bool VMAX>
-__global__ void __launch_bounds__(kBlock) k_filter_vmax_small(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundParams P) {
   constexpr int ITEMS = TileShape<D>::kItems;
-  constexpr uint32_t TILE = TileShape<D>::kTile;
-  __shared__ uint32_t s_cnt[ITEMS * kWarpsPerBlock];
-  __shared__ uint32_t s_seg;
+  constexpr uint32_t STEP = TileShape<D>::kStep;
+  __shared__ uint32_t s_warp[kWarpsPerBlock];
+  __shared__ uint32_t s_ticket;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -41,24 +43,26 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_small(const RoundParams 
   const uint8_t* __restrict__ mflag = P.mflag0;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t local_deact = 0;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t local_deact = 0, local_kept = 0;
   bool tie = false;
 
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_seg = atomicAdd(&c->ticket_f, 1u);
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&c->ticket_f, 1u);
     __syncthreads();
-    const uint32_t seg = s_seg;
-    if (seg >= P.nseg) break;
+    const uint32_t seg = s_ticket * kWarpsPerBlock + warp;
+    if (s_ticket * kWarpsPerBlock >= P.nseg) break;
+    if (seg >= P.nseg) continue;
     const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
     const uint32_t seg_base = seg * P.seg_cap;
     uint32_t out_off = 0;
-    for (uint32_t t0 = 0; t0 < cnt; t0 += TILE) {
+    for (uint32_t t0 = 0; t0 < cnt; t0 += STEP) {
       uint32_t e[ITEMS];
       bool survive[ITEMS];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t idx = t0 + k * kBlock + threadIdx.x;
+        const uint32_t idx = t0 + k * 32 + lane;
         survive[k] = false;
         e[k] = 0;
         if (idx < cnt) {
@@ -152,48 +156,34 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_small(const RoundParams 
         }
       }
       if (!out_ident) {
-        // order-preserving compaction of the tile: (item, warp) counts, then a short serial scan
-        uint32_t within[ITEMS];
+        // order-preserving warp compaction
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
           const uint32_t ballot = __ballot_sync(0xffffffffu, survive[k]);
-          within[k] = __popc(ballot & ((1u << lane) - 1u));
-          if (lane == 0) s_cnt[k * kWarpsPerBlock + warp] = __popc(ballot);
+          if (survive[k]) out[seg_base + out_off + __popc(ballot & lt_mask)] = e[k];
+          out_off += __popc(ballot);
         }
-        __syncthreads();
-        uint32_t run = 0, mine[ITEMS];
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-#pragma unroll
-          for (int w = 0; w < kWarpsPerBlock; ++w) {
-            if (w == static_cast<int>(warp)) mine[k] = run;
-            run += s_cnt[k * kWarpsPerBlock + w];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
-          if (survive[k]) out[seg_base + out_off + mine[k] + within[k]] = e[k];
-        out_off += run;
-        __syncthreads();
       }
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       const uint32_t kept = out_ident ? cnt : out_off;
       out_cnt[seg] = kept;
-      if (kept) atomicAdd(&c->active_small, kept);
+      local_kept += kept;
     }
   }
-  const uint32_t d = block_sum(local_deact, s_cnt);
+  const uint32_t d = block_sum(local_deact, s_warp);
   if (threadIdx.x == 0 && d) atomicAdd(P.deact_cnt + (r - 1), d);
+  const uint32_t kept = block_sum(local_kept, s_warp);
+  if (threadIdx.x == 0 && kept) atomicAdd(&c->active_small, kept);
   if (tie) c->tie_flag = 1u;
 }
 
 template <int D>
-__global__ void __launch_bounds__(kBlock) k_check_commit_small(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundParams P) {
   constexpr int ITEMS = TileShape<D>::kItems;
-  constexpr uint32_t TILE = TileShape<D>::kTile;
+  constexpr uint32_t STEP = TileShape<D>::kStep;
   __shared__ uint32_t s_warp[kWarpsPerBlock];
-  __shared__ uint32_t s_seg;
+  __shared__ uint32_t s_ticket;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
@@ -203,22 +193,24 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_small(const RoundParams
   const uint32_t* __restrict__ list_cnt = P.seg_cnt[par ^ 1];
   uint8_t* __restrict__ mflag = P.mflag0;
   const uint32_t tag = round_tag(P.ks, r);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t local_matched = 0;
 
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_seg = atomicAdd(&c->ticket_c, 1u);
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&c->ticket_c, 1u);
     __syncthreads();
-    const uint32_t seg = s_seg;
-    if (seg >= P.nseg) break;
+    const uint32_t seg = s_ticket * kWarpsPerBlock + warp;
+    if (s_ticket * kWarpsPerBlock >= P.nseg) break;
+    if (seg >= P.nseg) continue;
     const uint32_t cnt = list_cnt[seg];
     const uint32_t seg_base = seg * P.seg_cap;
-    for (uint32_t t0 = 0; t0 < cnt; t0 += TILE) {
+    for (uint32_t t0 = 0; t0 < cnt; t0 += STEP) {
       uint32_t e[ITEMS];
       bool valid[ITEMS], win[ITEMS];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t idx = t0 + k * kBlock + threadIdx.x;
+        const uint32_t idx = t0 + k * 32 + lane;
         valid[k] = idx < cnt;
         win[k] = false;
         e[k] = valid[k] ? (ident ? seg_base + idx : list[seg_base + idx]) : 0u;
@@ -283,7 +275,7 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_small(const RoundParams
       }
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (valid[k]) mflag[seg_base + t0 + k * kBlock + threadIdx.x] = win[k] ? 1 : 0;
+        if (valid[k]) mflag[seg_base + t0 + k * 32 + lane] = win[k] ? 1 : 0;
     }
   }
   const uint32_t t = block_sum(local_matched, s_warp);
