@@ -80,7 +80,8 @@ typedef struct {
   uint32_t flags;       /* HLM_B200_FLAG_* */
 } hlm_b200_config;
 
-#define HLM_B200_FLAG_NO_ROUND_OF 1u /* do not return matched_round */
+#define HLM_B200_FLAG_NO_ROUND_OF 1u   /* do not return matched_round */
+#define HLM_B200_FLAG_KERNEL_TIMES 2u  /* host loop only: CUDA-event time of every round kernel */
 
 /* hlm::MatchResult = Matching + RunReport (matching.hpp:15-48), flattened.  Arrays are owned by
  * the library; release with hlm_b200_result_free.  report.matched_per_round[r] is
@@ -103,6 +104,10 @@ typedef struct {
   uint32_t kernel_launches;        /* kernels of this library launched by the call */
   uint32_t graph_launches;         /* CUDA-graph launches (each runs many rounds) */
   uint32_t write_conflicts;        /* always 0 (RunReport::write_conflicts) */
+  /* HLM_B200_FLAG_KERNEL_TIMES: rounds + 1 entries each (the last filter launch finds the empty
+   * list); NULL otherwise.  filter = k_filter_vmax (all classes), check = k_check_commit. */
+  float* round_filter_ms;
+  float* round_check_ms;
 } hlm_b200_result;
 
 typedef struct hlm_b200_graph hlm_b200_graph; /* opaque: instance resident in HBM */
@@ -151,6 +156,9 @@ int hlm_b200_graph_info_get(const hlm_b200_graph* g, hlm_b200_graph_info* info);
 int hlm_b200_graph_download(hlm_b200_graph* g, uint64_t* vertex_offsets, uint32_t* vertex_incidence,
                             uint64_t* edge_offsets, uint32_t* edge_members, double* base_weights);
 void hlm_b200_graph_release(hlm_b200_graph* g);
+/* Runs all later work of this instance on the caller's CUDA stream (a cudaStream_t, e.g. the
+ * stream a framework is timing with its own events); NULL restores the instance's own stream. */
+int hlm_b200_graph_set_stream(hlm_b200_graph* g, void* cuda_stream);
 
 /* run_variant / local_max_crcw / local_max_crew (local_max_par.hpp:586,190,258) on a resident
  * instance.  Synchronous and re-entrant per graph handle. */

@@ -36,7 +36,8 @@ class Result(C.Structure):
                 ("device_edge_visits", C.c_uint64), ("device_pin_visits", C.c_uint64),
                 ("wall_time_ms", C.c_double), ("device_ms", C.c_double),
                 ("tie_redo_rounds", C.c_uint32), ("kernel_launches", C.c_uint32),
-                ("graph_launches", C.c_uint32), ("write_conflicts", C.c_uint32)]
+                ("graph_launches", C.c_uint32), ("write_conflicts", C.c_uint32),
+                ("round_filter_ms", C.POINTER(C.c_float)), ("round_check_ms", C.POINTER(C.c_float))]
 
 
 class GraphInfo(C.Structure):
@@ -62,6 +63,7 @@ SYMBOLS = {
     "hlm_b200_graph_info_get": (C.c_int, [C.c_void_p, C.POINTER(GraphInfo)]),
     "hlm_b200_graph_download": (C.c_int, [C.c_void_p] * 6),
     "hlm_b200_graph_release": (None, [C.c_void_p]),
+    "hlm_b200_graph_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hlm_b200_match": (C.c_int, [C.c_void_p, C.POINTER(Stream), C.POINTER(Config), C.POINTER(Result)]),
     "hlm_b200_match_host": (C.c_int, [C.POINTER(CsrView), C.POINTER(Stream), C.POINTER(Config), C.c_int,
                                       C.POINTER(Result)]),

@@ -84,6 +84,7 @@ class ParallelConfig:
     loop_mode: str = "auto"   # B200 extension: "host" | "graph"
     tie_mode: str = "auto"    # B200 extension: "exact" forces the three-level comparator
     want_round_of: bool = True
+    kernel_times: bool = False  # B200 extension (host loop): CUDA-event time of each round kernel
 
     def _c(self) -> _lib.Config:
         if isinstance(self.variant, str):
@@ -92,8 +93,8 @@ class ParallelConfig:
             variant = VARIANTS[self.variant]
         else:
             variant = int(self.variant)
-        return _lib.Config(variant, self.max_rounds, LOOP_MODES[self.loop_mode], TIE_MODES[self.tie_mode],
-                           0 if self.want_round_of else 1)
+        flags = (0 if self.want_round_of else 1) | (2 if self.kernel_times else 0)
+        return _lib.Config(variant, self.max_rounds, LOOP_MODES[self.loop_mode], TIE_MODES[self.tie_mode], flags)
 
 
 @dataclass
@@ -129,6 +130,8 @@ class RunReport:
     kernel_launches: int = 0
     graph_launches: int = 0
     _matched_edges: Optional[np.ndarray] = None
+    round_filter_ms: Optional[List[float]] = None
+    round_check_ms: Optional[List[float]] = None
 
     @property
     def matched_per_round(self) -> List[np.ndarray]:
@@ -185,7 +188,9 @@ def _convert(status: int, res: _lib.Result) -> MatchResult:
                            WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits)),
                            float(res.wall_time_ms), int(res.write_conflicts), float(res.device_ms),
                            int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
-                           int(res.graph_launches), matched)
+                           int(res.graph_launches), matched,
+                           _take(res.round_filter_ms, res.rounds + 1, np.float32).tolist() if res.round_filter_ms else None,
+                           _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None)
     finally:
         lib.hlm_b200_result_free(C.byref(res))
     if status == _lib.ERR_ROUND_LIMIT:
@@ -289,6 +294,11 @@ class DeviceHypergraph:
         if st != _lib.OK:
             _raise(st, "hlm_b200_verify")
         return VerificationReport(bool(dis.value), bool(mx.value), float(w.value))
+
+    def set_stream(self, cuda_stream: Optional[int]):
+        """Run this instance's work on the given cudaStream_t handle (e.g.
+        ``torch.cuda.current_stream().cuda_stream``) so the caller's events bracket it."""
+        _lib.load_library().hlm_b200_graph_set_stream(self._h, cuda_stream)
 
     def release(self):
         if self._h:

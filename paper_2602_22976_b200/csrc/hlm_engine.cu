@@ -128,7 +128,7 @@ Graph::~Graph() {
   dev_free(large_list);
   dev_free(voff);
   dev_free(vinc);
-  if (stream) cudaStreamDestroy(stream);
+  if (own_stream) cudaStreamDestroy(own_stream);
 }
 
 EdgeCsr Graph::csr() const {
@@ -161,7 +161,8 @@ static int init_device(Graph* g, int device) {
   CU_CHECK(cudaSetDevice(device));
   g->device = device;
   CU_CHECK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
-  CU_CHECK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  CU_CHECK(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  g->stream = g->own_stream;
   return HLM_B200_OK;
 }
 
@@ -633,6 +634,11 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
 
   Ctrl c = c0;
   uint32_t tie_redo = 0, graph_launches = 0;
+  const bool want_times = (cfg->flags & HLM_B200_FLAG_KERNEL_TIMES) && !use_graph && !L.exact;
+  std::vector<float> t_filter, t_check;
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  if (want_times)
+    for (auto& ev : tev) CU_CHECK(cudaEventCreate(&ev));
   if (g->m == 0) {
     c.status = ST_DONE;
   } else {
@@ -648,12 +654,22 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
         if (c.round <= max_rounds) ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
         L.advance(s, 0, 0);
       } else {
+        if (want_times) CU_CHECK(cudaEventRecord(tev[0], s));
         L.filter<true>(s);
+        if (want_times) CU_CHECK(cudaEventRecord(tev[1], s));
         L.check(s);
+        if (want_times) CU_CHECK(cudaEventRecord(tev[2], s));
         L.advance(s, 0, 0);
       }
       CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
       CU_CHECK(cudaStreamSynchronize(s));
+      if (want_times) {
+        float a = 0.f, b = 0.f;
+        CU_CHECK(cudaEventElapsedTime(&a, tev[0], tev[1]));
+        CU_CHECK(cudaEventElapsedTime(&b, tev[1], tev[2]));
+        t_filter.push_back(a);
+        t_check.push_back(b);
+      }
       if (c.status == ST_RUNNING) continue;
       if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
       if (c.status == ST_TIE) {
@@ -680,6 +696,16 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   out->device_edge_visits = c.edges_swept;
   // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
   out->kernel_launches = L.launches + (use_graph ? (rounds + 1) * w.graph_body_launches : 0);
+  for (auto& ev : tev)
+    if (ev) cudaEventDestroy(ev);
+  if (want_times) {
+    out->round_filter_ms = static_cast<float*>(std::calloc(rounds + 2, sizeof(float)));
+    out->round_check_ms = static_cast<float*>(std::calloc(rounds + 2, sizeof(float)));
+    for (size_t i = 0; i < t_filter.size() && i < rounds + 1u; ++i) {
+      out->round_filter_ms[i] = t_filter[i];
+      out->round_check_ms[i] = t_check[i];
+    }
+  }
   int rc = assemble_result(g, rounds, cfg, HLM_B200_VARIANT_CRCW, out);
   if (rc != HLM_B200_OK) return rc;
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
@@ -960,6 +986,15 @@ int hlm_b200_graph_download(hlm_b200_graph* gh, uint64_t* vertex_offsets, uint32
 
 void hlm_b200_graph_release(hlm_b200_graph* g) { delete reinterpret_cast<Graph*>(g); }
 
+int hlm_b200_graph_set_stream(hlm_b200_graph* gh, void* cuda_stream) {
+  if (!gh) return HLM_B200_ERR_INPUT;
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  cudaSetDevice(g->device);
+  cudaStreamSynchronize(g->stream);
+  g->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : g->own_stream;
+  return HLM_B200_OK;
+}
+
 int hlm_b200_match(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
                    hlm_b200_result* out) {
   if (!out) return HLM_B200_ERR_INPUT;
@@ -984,6 +1019,8 @@ void hlm_b200_result_free(hlm_b200_result* r) {
   std::free(r->matched_round);
   std::free(r->per_round_matched);
   std::free(r->per_round_deactivated);
+  std::free(r->round_filter_ms);
+  std::free(r->round_check_ms);
   std::memset(r, 0, sizeof(*r));
 }
 

@@ -61,6 +61,7 @@ struct Graph {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
   uint32_t n = 0, m = 0;
   uint32_t id_base = 0;  // global id of local edge 0 (edge shard of a larger instance)
   uint64_t kappa = 0;
