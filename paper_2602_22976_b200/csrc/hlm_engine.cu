@@ -71,7 +71,7 @@ template <typename T>
 static int dev_alloc(T** p, size_t count, Graph* g) {
   *p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  cudaError_t e = pool_malloc(reinterpret_cast<void**>(p), count * sizeof(T));
   if (e != cudaSuccess) {
     set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? HLM_B200_ERR_NOMEM : HLM_B200_ERR_CUDA;
@@ -80,9 +80,37 @@ static int dev_alloc(T** p, size_t count, Graph* g) {
   return HLM_B200_OK;
 }
 
-static void dev_free(void* p) {
-  if (p) cudaFree(p);
+static cudaStream_t g_alloc_stream[64] = {};
+
+static cudaStream_t alloc_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!g_alloc_stream[dev]) {
+    cudaStreamCreateWithFlags(&g_alloc_stream[dev], cudaStreamNonBlocking);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return g_alloc_stream[dev];
 }
+
+cudaError_t pool_malloc(void** p, size_t bytes) {
+  cudaStream_t s = alloc_stream();
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);  // the block is usable from every stream once this returns
+}
+
+void pool_free(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();  // frees are rare and never inside the round loop
+  cudaFreeAsync(p, alloc_stream());
+}
+
+static void dev_free(void* p) { pool_free(p); }
 
 void Workspace::release() {
   dev_free(ctrl);
@@ -181,19 +209,19 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins) {
   }
   CU_CHECK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, s));
   CU_CHECK(cudaStreamSynchronize(s));
-  cudaFree(d_st);
+  pool_free(d_st);
   if (st.bad_offsets) {
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
     set_error("edge_offsets are not monotone");
     return HLM_B200_ERR_INPUT;
   }
   if (m && st.min_size == 0) {
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
     set_error("an edge is empty (hypergraph.hpp:91)");
     return HLM_B200_ERR_INPUT;
   }
   if (check_pins && g->kappa && st.max_pin >= g->n) {
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
     set_error("vertex id %u out of range [0, %u)", st.max_pin, g->n);
     return HLM_B200_ERR_INPUT;
   }
@@ -201,14 +229,14 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins) {
   g->num_large = st.num_large;
   if (m && st.min_size == st.max_size) {
     g->uniform_d = st.max_size;
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
   } else if (m == 0) {
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
   } else if (g->kappa < (1ull << 32)) {
     ST_CHECK(dev_alloc(&g->off32, static_cast<size_t>(m) + 1, g));
     k_narrow_offsets<<<grid_for(g, m + 1ull), kBlock, 0, s>>>(off64_dev, g->off32, m + 1ull);
     CU_CHECK(cudaStreamSynchronize(s));
-    cudaFree(off64_dev);
+    pool_free(off64_dev);
   } else {
     g->off64 = off64_dev;
     g->device_bytes += (static_cast<size_t>(m) + 1) * 8;
@@ -220,7 +248,7 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins) {
     CU_CHECK(cudaMemsetAsync(d_cnt, 0, 4, s));
     k_collect_large<<<grid_for(g, m), kBlock, 0, s>>>(g->csr(), m, g->large_list, d_cnt);
     CU_CHECK(cudaStreamSynchronize(s));
-    cudaFree(d_cnt);
+    pool_free(d_cnt);
   }
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
@@ -240,7 +268,7 @@ int finish_weights(Graph* g) {
   g->base_integral = !ws.non_integer;
   if (ws.min_bits == ws.max_bits) {
     g->base_const = g->base_min;
-    cudaFree(g->base);
+    pool_free(g->base);
     g->device_bytes -= static_cast<size_t>(g->m) * 8;
     g->base = nullptr;
   }
@@ -255,7 +283,7 @@ int weight_stats(Graph* g, double lo, WeightStats* out) {
   k_weight_stats<<<grid_for(g, g->m), kBlock, 0, g->stream>>>(g->base, g->m, lo, d);
   CU_CHECK(cudaMemcpyAsync(out, d, sizeof(*out), cudaMemcpyDeviceToHost, g->stream));
   CU_CHECK(cudaStreamSynchronize(g->stream));
-  cudaFree(d);
+  pool_free(d);
   return HLM_B200_OK;
 }
 
@@ -312,7 +340,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out) {
   }
   if (e != cudaSuccess) {
     set_error("host-to-device copy failed: %s", cudaGetErrorString(e));
-    cudaFree(off64);
+    pool_free(off64);
     return fail(HLM_B200_ERR_CUDA);
   }
   g->h2d_bytes = (static_cast<uint64_t>(m) + 1) * 8 + g->kappa * 4 + static_cast<uint64_t>(m) * 8;

@@ -88,6 +88,12 @@ struct Graph {
   ~Graph();
 };
 
+// HBM allocations go through the device's stream-ordered pool with an unlimited release
+// threshold: a freed instance's memory stays mapped and the next upload reuses it (plain
+// cudaMalloc after a multi-GB cudaFree costs ~0.1 s per GB on this platform).
+cudaError_t pool_malloc(void** p, size_t bytes);
+void pool_free(void* p);
+
 void set_error(const char* fmt, ...);
 uint32_t default_max_rounds(uint32_t m);
 int new_graph(int device, Graph** out);

@@ -30,7 +30,7 @@ template <typename T>
 static int dalloc(T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  cudaError_t e = pool_malloc(reinterpret_cast<void**>(p), count * sizeof(T));
   if (e != cudaSuccess) {
     set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? HLM_B200_ERR_NOMEM : HLM_B200_ERR_CUDA;
@@ -145,7 +145,7 @@ int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out
   CU_CHECK(cudaStreamSynchronize(s));
   CU_CHECK(cudaMemcpyAsync(out + count, &tot, 8, cudaMemcpyHostToDevice, s));
   CU_CHECK(cudaStreamSynchronize(s));
-  cudaFree(sums);
+  pool_free(sums);
   CU_CHECK(cudaGetLastError());
   if (total) *total = tot;
   return HLM_B200_OK;
@@ -185,7 +185,7 @@ int build_incidence(Graph* g) {
   if (g->kappa) k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, deg);
   int rc = device_exclusive_scan_u32_to_u64(g, deg, g->voff, g->n, nullptr);
   if (rc != HLM_B200_OK) {
-    cudaFree(deg);
+    pool_free(deg);
     return rc;
   }
   CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
@@ -193,7 +193,7 @@ int build_incidence(Graph* g) {
     k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(
         g->csr(), g->m, reinterpret_cast<const unsigned long long*>(g->voff), deg, g->vinc);
   CU_CHECK(cudaStreamSynchronize(s));
-  cudaFree(deg);
+  pool_free(deg);
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
 }
@@ -360,7 +360,7 @@ int generate(const hlm_b200_syn_spec* spec, int device, Graph** out) {
     g->device_bytes += g->kappa * 4;
     k_syn_pins<<<grid_of(g, m_local), kBlock, 0, s>>>(p, nullptr, g->pins);
     // uniform instances never materialise offsets
-    cudaFree(off64);
+    pool_free(off64);
     g->uniform_d = d;
     g->max_edge_size = d;
     g->num_large = d > kLargeEdge ? m_local : 0;
@@ -373,13 +373,13 @@ int generate(const hlm_b200_syn_spec* spec, int device, Graph** out) {
     if ((rc = dalloc(&sizes, m_local)) != HLM_B200_OK) return fail(rc);
     k_syn_sizes<<<grid_of(g, m_local), kBlock, 0, s>>>(p, sizes);
     rc = device_exclusive_scan_u32_to_u64(g, sizes, off64, m_local, &g->kappa);
-    cudaFree(sizes);
+    pool_free(sizes);
     if (rc != HLM_B200_OK) {
-      cudaFree(off64);
+      pool_free(off64);
       return fail(rc);
     }
     if ((rc = dalloc(&g->pins, g->kappa)) != HLM_B200_OK) {
-      cudaFree(off64);
+      pool_free(off64);
       return fail(rc);
     }
     g->device_bytes += g->kappa * 4;
@@ -434,7 +434,7 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
     k_widen_offsets<<<grid_of(g, g->m + 1ull), kBlock, 0, s>>>(g->csr(), g->m, tmp);
     CU_CHECK(cudaMemcpyAsync(eoff, tmp, (static_cast<size_t>(g->m) + 1) * 8, cudaMemcpyDeviceToHost, s));
     CU_CHECK(cudaStreamSynchronize(s));
-    cudaFree(tmp);
+    pool_free(tmp);
   }
   if (pins && g->kappa) CU_CHECK(cudaMemcpyAsync(pins, g->pins, g->kappa * 4, cudaMemcpyDeviceToHost, s));
   if (base && g->m) {
@@ -446,7 +446,7 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
       k_fill_const<<<grid_of(g, g->m), kBlock, 0, s>>>(tmp, g->m, g->base_const);
       CU_CHECK(cudaMemcpyAsync(base, tmp, static_cast<size_t>(g->m) * 8, cudaMemcpyDeviceToHost, s));
       CU_CHECK(cudaStreamSynchronize(s));
-      cudaFree(tmp);
+      pool_free(tmp);
     }
   }
   if (voff || vinc) {
