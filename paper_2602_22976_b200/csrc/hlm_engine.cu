@@ -53,6 +53,11 @@ static uint64_t dbits(double d) {
   return u;
 }
 
+bool reorder_enabled() {
+  const char* env = std::getenv("HLM_B200_REORDER");
+  return !(env && env[0] == '0');
+}
+
 uint32_t default_max_rounds(uint32_t m) {  // matching.hpp:87-89, common.hpp:27-35
   const uint64_t x = static_cast<uint64_t>(m) + 2;
   uint32_t r = 0;
@@ -115,6 +120,7 @@ static void dev_free(void* p) { pool_free(p); }
 void Workspace::release() {
   dev_free(ctrl);
   dev_free(vkey);
+  dev_free(vtop);
   dev_free(dead);
   dev_free(mround);
   dev_free(mbits);
@@ -154,6 +160,8 @@ Graph::~Graph() {
   dev_free(off64);
   dev_free(base);
   dev_free(large_list);
+  dev_free(orig);
+  dev_free(base_run);
   dev_free(voff);
   dev_free(vinc);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -346,6 +354,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out) {
   g->h2d_bytes = (static_cast<uint64_t>(m) + 1) * 8 + g->kappa * 4 + static_cast<uint64_t>(m) * 8;
   if ((rc = finish_graph(g, off64, true)) != HLM_B200_OK) return fail(rc);
   if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
+  if (reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
   *out = g;
   return HLM_B200_OK;
 }
@@ -358,6 +367,7 @@ static int ensure_workspace(Graph* g, uint32_t max_rounds) {
   if (!w.ctrl) {
     ST_CHECK(dev_alloc(&w.ctrl, 1, g));
     ST_CHECK(dev_alloc(&w.vkey, g->n, g));
+    ST_CHECK(dev_alloc(&w.vtop, g->n, g));
     ST_CHECK(dev_alloc(&w.dead, (static_cast<size_t>(g->n) + 31) / 32, g));
     ST_CHECK(dev_alloc(&w.mround, g->m, g));
     w.mbits_words = (g->m + 31) / 32;
@@ -444,7 +454,7 @@ static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_roun
     ks->payload_bits = 64 - tag_bits;
     ks->hash_bits = ks->payload_bits - qb;
     ks->wq_min = wq_min;
-    ks->tag_period = (1u << tag_bits) - 1u;
+    ks->tag_period = (1u << tag_bits) - 2u;  // the all-ones tag is kVertexDead
     return HLM_B200_OK;
   }
   const uint64_t span = dbits(wmax) - dbits(wmin);
@@ -452,7 +462,7 @@ static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_roun
   ks->payload_bits = std::max(1, bitlen64(span));
   ks->wmin_bits = dbits(wmin);
   const int tag_bits = 64 - ks->payload_bits;
-  ks->tag_period = tag_bits >= 16 ? 65535u : ((1u << tag_bits) - 1u);
+  ks->tag_period = tag_bits >= 16 ? 65534u : (tag_bits >= 2 ? (1u << tag_bits) - 2u : 0u);  // 0: no fast path
   return HLM_B200_OK;
 }
 
@@ -600,7 +610,8 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   RoundParams& P = L.P;
   std::memset(&P, 0, sizeof(P));
   P.csr = g->csr();
-  P.base = g->base;
+  P.base = g->orig ? g->base_run : g->base;
+  P.orig = g->orig;
   P.base_const = g->base_const;
   P.n = g->n;
   P.m = g->m;
@@ -613,11 +624,16 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   P.stream.hi = st->noise_high;
   P.stream.width = st->noise_high - st->noise_low;
   ST_CHECK(choose_key_scheme(g, P.stream, max_rounds, &P.ks));
+  if (P.ks.tag_period == 0) {  // weights span too many binades for a tagged 64-bit key
+    L.exact = true;
+    P.ks.tag_period = 65534u;
+  }
   // the load-before-atomic filter pays off once a vertex sees many edges per round
   P.ks.precheck = (g->n && g->kappa / g->n >= 6) ? 1u : 0u;
   if (const char* env = std::getenv("HLM_B200_PRECHECK")) P.ks.precheck = env[0] == '1';
   P.ctrl = w.ctrl;
   P.vkey = w.vkey;
+  P.vtop = w.vtop;
   P.dead = w.dead;
   P.mbits = w.mbits;
   P.mround = w.mround;
@@ -652,6 +668,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   c0.max_rounds = max_rounds;
   CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
   CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+  CU_CHECK(cudaMemsetAsync(w.vtop, 0, static_cast<size_t>(g->n) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
@@ -714,7 +731,10 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
           return HLM_B200_ERR_CUDA;
         }
       }
-      if (c.status == ST_EPOCH) CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+      if (c.status == ST_EPOCH) {
+        k_epoch_reset<<<grid_for(g, g->n), kBlock, 0, s>>>(w.vkey, w.vtop, g->n);
+        ++L.launches;
+      }
     }
   }
   CU_CHECK(cudaGetLastError());
@@ -912,18 +932,20 @@ static int verify(Graph* g, const uint32_t* matched, uint64_t count, int* disjoi
     CU_CHECK(cudaMemsetAsync(inm, 0, mw * 4, s));
     CU_CHECK(cudaMemsetAsync(d_out, 0, sizeof(VerifyOut), s));
     if (count)
-      k_verify_cover<<<grid_for(g, count, kWarpsPerBlock), kBlock, 0, s>>>(g->csr(), g->m, d_ids, count,
-                                                                          covered, inm, d_out);
+      k_verify_mark<<<grid_for(g, count), kBlock, 0, s>>>(d_ids, count, g->m, g->id_base, inm, d_out);
     CU_CHECK(cudaMemcpyAsync(&vo, d_out, sizeof(vo), cudaMemcpyDeviceToHost, s));
     CU_CHECK(cudaStreamSynchronize(s));
     if (vo.out_of_range) {
       set_error("matching references an edge out of range");
       return HLM_B200_ERR_INPUT;
     }
-    if (g->m) k_verify_maximal<<<grid_for(g, g->m), kBlock, 0, s>>>(g->csr(), g->m, covered, inm, d_out);
+    if (g->m) {
+      k_verify_sweep<1><<<grid_for(g, g->m), kBlock, 0, s>>>(g->csr(), g->m, g->orig, covered, inm, d_out);
+      k_verify_sweep<2><<<grid_for(g, g->m), kBlock, 0, s>>>(g->csr(), g->m, g->orig, covered, inm, d_out);
+    }
     if (g->base && count) {
       ST_CHECK(dev_alloc(&d_w, count, nullptr));
-      k_gather_weights<<<grid_for(g, count), kBlock, 0, s>>>(g->base, d_ids, count, d_w);
+      k_gather_weights<<<grid_for(g, count), kBlock, 0, s>>>(g->base, d_ids, g->id_base, count, d_w);
       wts.resize(count);
       CU_CHECK(cudaMemcpyAsync(wts.data(), d_w, count * 8, cudaMemcpyDeviceToHost, s));
     }

@@ -14,6 +14,7 @@ struct Graph;
 struct Workspace {
   Ctrl* ctrl = nullptr;
   unsigned long long* vkey = nullptr;
+  uint32_t* vtop = nullptr;
   uint32_t* dead = nullptr;
   uint16_t* mround = nullptr;
   uint32_t* mbits = nullptr;
@@ -72,7 +73,9 @@ struct Graph {
   uint32_t max_edge_size = 0;
   uint32_t num_large = 0;
   uint32_t* large_list = nullptr;
-  double* base = nullptr;  // null: all weights equal base_const
+  double* base = nullptr;  // null: all weights equal base_const (caller's edge order)
+  uint32_t* orig = nullptr;     // resident edge e is the caller's edge orig[e] (null: same order)
+  double* base_run = nullptr;   // base weights in resident order when orig != null
   double base_const = 1.0;
   double base_min = 1.0, base_max = 1.0;
   bool base_integral = true;  // every base weight is an integer below 2^32 (order-free exact sums)
@@ -101,6 +104,9 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins);
 int finish_weights(Graph* g);
 int weight_stats(Graph* g, double lo, WeightStats* out);
 int build_incidence(Graph* g);
+bool reorder_enabled();
+int reorder_by_first_pin(Graph* g);
+int download_pins_original_order(Graph* g, uint32_t* host_pins);
 int generate(const hlm_b200_syn_spec* spec, int device, Graph** out);
 int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base);
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);

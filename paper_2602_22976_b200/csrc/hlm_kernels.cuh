@@ -76,13 +76,29 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (survive[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
-        if (r > 1) {
+        // One L2 load per pin serves two purposes: kVertexDead in the slot means the vertex was
+        // covered by a matched edge (invalidation, local_max_par.hpp:229-248), anything else is
+        // the running maximum that filters the atomics below.
+        const bool peek = r > 1 || P.ks.precheck;
+        uint32_t cur[ITEMS][D];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) cur[k][i] = 0u;
+        }
+        if (peek) {
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k)
+            if (survive[k]) {
+#pragma unroll
+              for (int i = 0; i < D; ++i) cur[k][i] = __ldcg(P.vtop + pv[k].v[i]);
+            }
 #pragma unroll
           for (int k = 0; k < ITEMS; ++k) {
             if (!survive[k]) continue;
             bool dead_any = false;
 #pragma unroll
-            for (int i = 0; i < D; ++i) dead_any |= vertex_dead(P.dead, pv[k].v[i]);
+            for (int i = 0; i < D; ++i) dead_any |= (cur[k][i] == kTopDead);
             if (dead_any) {
               survive[k] = false;
               ++local_deact;
@@ -90,41 +106,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
           }
         }
         if constexpr (VMAX) {
-          unsigned long long key[ITEMS];
 #pragma unroll
           for (int k = 0; k < ITEMS; ++k)
-            if (survive[k])
-              key[k] = priority_key(P.stream, P.ks, e[k] + P.id_base, r, base_of(P, e[k]), tag);
-          if (P.ks.precheck) {
-            unsigned long long cur[ITEMS][D];
+            if (survive[k]) {
+              const unsigned long long key =
+                  priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k)
-              if (survive[k]) {
-#pragma unroll
-                for (int i = 0; i < D; ++i) cur[k][i] = __ldcg(P.vkey + pv[k].v[i]);
-              }
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k)
-              if (survive[k]) {
-#pragma unroll
-                for (int i = 0; i < D; ++i) {
-                  if (cur[k][i] < key[k])
-                    tie |= (atomicMax(P.vkey + pv[k].v[i], key[k]) == key[k]);
-                  else
-                    tie |= (cur[k][i] == key[k]);
-                }
-              }
-          } else {
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k)
-              if (survive[k]) {
-                unsigned long long old[D];
-#pragma unroll
-                for (int i = 0; i < D; ++i) old[i] = atomicMax(P.vkey + pv[k].v[i], key[k]);
-#pragma unroll
-                for (int i = 0; i < D; ++i) tie |= (old[i] == key[k]);
-              }
-          }
+              for (int i = 0; i < D; ++i) tie |= deposit_key(P, pv[k].v[i], key, cur[k][i]);
+            }
         }
       } else {
         // runtime sizes: ITEMS == 1
@@ -138,18 +127,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
             const uint32_t* __restrict__ pp = P.csr.pins + b;
             bool dead_any = false;
             if (r > 1)
-              for (uint32_t i = 0; i < s; ++i) dead_any |= vertex_dead(P.dead, __ldg(pp + i));
+              for (uint32_t i = 0; i < s; ++i) dead_any |= (__ldcg(P.vtop + __ldg(pp + i)) == kTopDead);
             if (dead_any) {
               survive[0] = false;
               ++local_deact;
             } else if constexpr (VMAX) {
               const unsigned long long key =
-                  priority_key(P.stream, P.ks, e[0] + P.id_base, r, base_of(P, e[0]), tag);
-              if (P.ks.precheck) {
-                for (uint32_t i = 0; i < s; ++i) tie |= vertex_max(P.vkey + __ldg(pp + i), key);
-              } else {
-                for (uint32_t i = 0; i < s; ++i)
-                  tie |= (atomicMax(P.vkey + __ldg(pp + i), key) == key);
+                  priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
+              const bool peek = r > 1 || P.ks.precheck;
+              for (uint32_t i = 0; i < s; ++i) {
+                const uint32_t v = __ldg(pp + i);
+                tie |= deposit_key(P, v, key, peek ? __ldcg(P.vtop + v) : 0u);
               }
             }
           }
@@ -217,36 +205,47 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
-        unsigned long long key[ITEMS], top[ITEMS];
+        unsigned long long key[ITEMS];
+        uint32_t top[ITEMS];
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (valid[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
-        // first pin of every item in flight together; most edges lose right here
+        // 32-bit filter word of the first pin of every item in flight together; most edges lose
+        // right here (and with the edges sorted by first pin these loads are coalesced)
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-          if (valid[k]) top[k] = __ldg(P.vkey + pv[k].v[0]);
+          if (valid[k]) top[k] = __ldcg(P.vtop + pv[k].v[0]);
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (valid[k]) {
-            key[k] = priority_key(P.stream, P.ks, e[k] + P.id_base, r, base_of(P, e[k]), tag);
-            win[k] = top[k] == key[k];
+            key[k] = priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
+            win[k] = top[k] == static_cast<uint32_t>(key[k] >> 32);
           }
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (win[k]) {
-            unsigned long long rest[D];
+            uint32_t rest[D];
 #pragma unroll
-            for (int i = 1; i < D; ++i) rest[i] = __ldg(P.vkey + pv[k].v[i]);
+            for (int i = 1; i < D; ++i) rest[i] = __ldcg(P.vtop + pv[k].v[i]);
 #pragma unroll
-            for (int i = 1; i < D; ++i) win[k] &= (rest[i] == key[k]);
+            for (int i = 1; i < D; ++i) win[k] &= (rest[i] == static_cast<uint32_t>(key[k] >> 32));
+          }
+        // the few survivors of the 32-bit filter are confirmed against the full keys
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (win[k]) {
+            unsigned long long full[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) full[i] = __ldcg(P.vkey + pv[k].v[i]);
+#pragma unroll
+            for (int i = 0; i < D; ++i) win[k] &= (full[i] == key[k]);
           }
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (win[k]) {
-            P.mround[e[k]] = static_cast<uint16_t>(r);
-            atomicOr(P.mbits + (e[k] >> 5), 1u << (e[k] & 31));
+            mark_matched(P, e[k], r);
 #pragma unroll
-            for (int i = 0; i < D; ++i) atomicOr(P.dead + (pv[k].v[i] >> 5), 1u << (pv[k].v[i] & 31));
+            for (int i = 0; i < D; ++i) mark_dead(P, pv[k].v[i]);
             ++local_matched;
           }
       } else {
@@ -257,15 +256,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
           if (!(P.has_large && s > kLargeEdge)) {
             const uint32_t* __restrict__ pp = P.csr.pins + b;
             const unsigned long long key =
-                priority_key(P.stream, P.ks, e[0] + P.id_base, r, base_of(P, e[0]), tag);
+                priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
             bool w = true;
-            for (uint32_t i = 0; i < s && w; ++i) w = (__ldg(P.vkey + __ldg(pp + i)) == key);
+            for (uint32_t i = 0; i < s && w; ++i) w = key_wins_at(P, __ldg(pp + i), key);
             if (w) {
-              P.mround[e[0]] = static_cast<uint16_t>(r);
-              atomicOr(P.mbits + (e[0] >> 5), 1u << (e[0] & 31));
+              mark_matched(P, e[0], r);
               for (uint32_t i = 0; i < s; ++i) {
                 const uint32_t v = __ldg(pp + i);
-                atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+                mark_dead(P, v);
               }
               ++local_matched;
             }
@@ -309,7 +307,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
     const uint32_t* __restrict__ pp = P.csr.pins + b;
     bool dead_any = false;
     if (r > 1)
-      for (uint32_t i = lane; i < s; i += 32) dead_any |= vertex_dead(P.dead, __ldg(pp + i));
+      for (uint32_t i = lane; i < s; i += 32) dead_any |= (__ldcg(P.vtop + __ldg(pp + i)) == kTopDead);
     dead_any = __any_sync(0xffffffffu, dead_any);
     if (dead_any) {
       local_deact += (lane == 0);
@@ -317,8 +315,11 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
     }
     if (lane == 0) out[atomicAdd(&c->count1[par ^ 1], 1u)] = e;
     if constexpr (VMAX) {
-      const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
-      for (uint32_t i = lane; i < s; i += 32) tie |= vertex_max(P.vkey + __ldg(pp + i), key);
+      const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
+      for (uint32_t i = lane; i < s; i += 32) {
+        const uint32_t v = __ldg(pp + i);
+        tie |= deposit_key(P, v, key, __ldcg(P.vtop + v));
+      }
     }
   }
   if (local_deact) atomicAdd(P.deact_cnt + (r - 1), local_deact);
@@ -344,22 +345,21 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
     uint32_t s;
     P.csr.range(e, b, s);
     const uint32_t* __restrict__ pp = P.csr.pins + b;
-    const unsigned long long key = priority_key(P.stream, P.ks, e + P.id_base, r, base_of(P, e), tag);
+    const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
     bool win = true;
     for (uint32_t i0 = 0; i0 < s; i0 += 32) {
       const uint32_t i = i0 + lane;
-      const bool ok = i < s ? (__ldg(P.vkey + __ldg(pp + i)) == key) : true;
+      const bool ok = i < s ? key_wins_at(P, __ldg(pp + i), key) : true;
       win = __all_sync(0xffffffffu, ok);
       if (!win) break;  // first losing chunk ends the scan
     }
     if (win) {
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
-        atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+        mark_dead(P, v);
       }
       if (lane == 0) {
-        P.mround[e] = static_cast<uint16_t>(r);
-        atomicOr(P.mbits + (e >> 5), 1u << (e & 31));
+        mark_matched(P, e, r);
         ++local_matched;
       }
     }
@@ -395,6 +395,14 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
   }
   c->status = status;
   if (in_graph) cudaGraphSetConditional(handle, status == ST_RUNNING ? 1u : 0u);
+}
+
+// Round tags wrapped: forget every running maximum but keep the dead marks.
+__global__ void k_epoch_reset(unsigned long long* vkey, uint32_t* vtop, uint32_t n) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    vkey[v] = 0ull;
+    if (vtop[v] != kTopDead) vtop[v] = 0u;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -440,9 +448,9 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
     }
     const uint32_t* __restrict__ pp = P.csr.pins + b;
     const unsigned long long A = static_cast<unsigned long long>(
-        __double_as_longlong(edge_weight(P.stream, e + P.id_base, r, base_of(P, e))));
-    const unsigned long long B = tie_hash(P.stream, e + P.id_base, r);
-    const uint32_t C = e + P.id_base + 1u;
+        __double_as_longlong(edge_weight(P.stream, edge_gid(P, e), r, base_of(P, e))));
+    const unsigned long long B = tie_hash(P.stream, edge_gid(P, e), r);
+    const uint32_t C = edge_gid(P, e) + 1u;
     bool win = true;
     for (uint32_t i = lane; i < s; i += 32) {
       const uint32_t v = __ldg(pp + i);
@@ -461,11 +469,10 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
       if (win) {
         for (uint32_t i = lane; i < s; i += 32) {
           const uint32_t v = __ldg(pp + i);
-          atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+          mark_dead(P, v);
         }
         if (lane == 0) {
-          P.mround[e] = static_cast<uint16_t>(r);
-          atomicOr(P.mbits + (e >> 5), 1u << (e & 31));
+          mark_matched(P, e, r);
           ++local_matched;
         }
       }
@@ -677,55 +684,54 @@ struct VerifyOut {
   uint32_t pad;
 };
 
-__global__ void k_verify_cover(const EdgeCsr csr, uint32_t m, const uint32_t* matched, uint64_t count,
-                               uint32_t* covered, uint32_t* in_matching, VerifyOut* out) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = blockIdx.x * static_cast<uint64_t>(kWarpsPerBlock) + (threadIdx.x >> 5);
-  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
-  for (uint64_t k = warp; k < count; k += nwarps) {
-    const uint32_t e = matched[k];
-    if (e >= m) {
-      if (lane == 0) out->out_of_range = 1;
+// pass 0: bitmap of the caller's matched ids (a repeated id covers its vertices twice)
+__global__ void k_verify_mark(const uint32_t* matched, uint64_t count, uint32_t m, uint32_t id_base,
+                              uint32_t* in_matching, VerifyOut* out) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t id = matched[k] - id_base;
+    if (matched[k] < id_base || id >= m) {
+      out->out_of_range = 1;
       continue;
     }
-    if (lane == 0) atomicOr(in_matching + (e >> 5), 1u << (e & 31));
+    const uint32_t bit = 1u << (id & 31);
+    if (atomicOr(in_matching + (id >> 5), bit) & bit) out->overlap = 1;
+  }
+}
+
+// pass 1: matched edges cover their pins; pass 2: every other edge must touch a covered vertex
+template <int PASS>
+__global__ void k_verify_sweep(const EdgeCsr csr, uint32_t m, const uint32_t* orig, uint32_t* covered,
+                               const uint32_t* in_matching, VerifyOut* out) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint32_t id = orig ? orig[e] : e;
+    const bool in_m = (in_matching[id >> 5] >> (id & 31)) & 1u;
+    if (in_m != (PASS == 1)) continue;
     uint64_t b;
     uint32_t s;
     csr.range(e, b, s);
-    for (uint32_t i = lane; i < s; i += 32) {
-      const uint32_t v = csr.pins[b + i];
-      const uint32_t bit = 1u << (v & 31);
-      if (atomicOr(covered + (v >> 5), bit) & bit) out->overlap = 1;
+    if (PASS == 1) {
+      for (uint32_t i = 0; i < s; ++i) {
+        const uint32_t v = csr.pins[b + i];
+        const uint32_t bit = 1u << (v & 31);
+        if (atomicOr(covered + (v >> 5), bit) & bit) out->overlap = 1;
+      }
+    } else {
+      bool any = false;
+      for (uint32_t i = 0; i < s && !any; ++i) {
+        const uint32_t v = csr.pins[b + i];
+        any = (covered[v >> 5] >> (v & 31)) & 1u;
+      }
+      if (!any) out->addable = 1;
     }
   }
 }
 
-__global__ void k_verify_maximal(const EdgeCsr csr, uint32_t m, const uint32_t* covered,
-                                 const uint32_t* in_matching, VerifyOut* out) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
-  // 32 edges per warp iteration; lanes walk their own edge (sizes are small on average)
-  for (uint32_t e0 = warp * 32; e0 < m; e0 += nwarps * 32) {
-    const uint32_t e = e0 + lane;
-    if (e >= m) continue;
-    if ((in_matching[e >> 5] >> (e & 31)) & 1u) continue;
-    uint64_t b;
-    uint32_t s;
-    csr.range(e, b, s);
-    bool any = false;
-    for (uint32_t i = 0; i < s && !any; ++i) {
-      const uint32_t v = csr.pins[b + i];
-      any = (covered[v >> 5] >> (v & 31)) & 1u;
-    }
-    if (!any) out->addable = 1;
-  }
-}
-
-__global__ void k_gather_weights(const double* base, const uint32_t* ids, uint64_t count, double* out) {
+__global__ void k_gather_weights(const double* base, const uint32_t* ids, uint32_t id_base, uint64_t count,
+                                 double* out) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    out[i] = base[ids[i]];
+    out[i] = base[ids[i] - id_base];
 }
 
 }  // namespace hlmb

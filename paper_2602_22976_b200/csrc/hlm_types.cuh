@@ -84,10 +84,13 @@ struct RoundParams {
   uint32_t m;
   uint32_t has_large;  // some edges have more than kLargeEdge pins
   uint32_t id_base;    // global id of local edge 0 (edge shards); priorities use global ids
+  const uint32_t* orig;  // null, or: resident edge e is the caller's edge orig[e] (the loader
+                         // sorted the edges by first pin so that pin-0 accesses are coalesced)
   StreamParams stream;
   KeyScheme ks;
   Ctrl* ctrl;
-  unsigned long long* vkey;  // n round-tagged vertex maxima
+  unsigned long long* vkey;  // n round-tagged vertex maxima (full 64-bit keys)
+  uint32_t* vtop;            // n: high word of vkey, or kTopDead; the L2-resident filter array
   uint32_t* dead;            // n bits: vertex covered by a matched edge
   uint32_t* mbits;           // m bits: edge matched
   uint16_t* mround;          // m: round an edge matched in (valid where its mbits bit is set)
@@ -104,8 +107,58 @@ struct RoundParams {
   uint32_t* deact_cnt;       // [round] edges deactivated in that round
 };
 
+// vtop[v] mirrors the high 32 bits of vkey[v] (round tag + the leading payload bits).  It is half
+// the size of vkey, so it stays L2-resident where vkey would spill to HBM as random 32-byte
+// sectors, and almost every decision is made on it: an edge whose high word is below vtop[v]
+// cannot be the maximum at v (no atomic needed), an edge whose high word differs from vtop[v]
+// after the vertex-max pass lost at v (no 64-bit compare needed).  A vertex covered by a matched
+// edge keeps kTopDead there for the rest of the run: larger than every key's high word (the
+// all-ones tag is reserved), so atomicMax never disturbs it, and the same load that filters the
+// atomics tells the filter kernel that the edge must be dropped.
+constexpr uint32_t kTopDead = 0xFFFFFFFFu;
+
 __device__ __forceinline__ bool vertex_dead(const uint32_t* dead, uint32_t v) {
   return (__ldg(dead + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+// The id the reference knows an edge by: keys, tie hashes and results always use it.
+__device__ __forceinline__ uint32_t edge_local_id(const RoundParams& P, uint32_t e) {
+  return P.orig ? __ldg(P.orig + e) : e;
+}
+__device__ __forceinline__ uint32_t edge_gid(const RoundParams& P, uint32_t e) {
+  return edge_local_id(P, e) + P.id_base;
+}
+
+// matched edges record their round and set their bit in the (caller-id indexed) matched bitmap
+__device__ __forceinline__ void mark_matched(const RoundParams& P, uint32_t e, uint32_t r) {
+  const uint32_t id = edge_local_id(P, e);
+  P.mround[id] = static_cast<uint16_t>(r);
+  atomicOr(P.mbits + (id >> 5), 1u << (id & 31));
+}
+
+// completion marking (local_max_par.hpp:221): matched edges are vertex-disjoint, so the key
+// store is exclusive; the bitmap copy feeds verification and the multi-GPU dead-bit exchange.
+__device__ __forceinline__ void mark_dead(const RoundParams& P, uint32_t v) {
+  P.vtop[v] = kTopDead;
+  atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+}
+
+// vkey[v] = max(vkey[v], key), vtop[v] = max(vtop[v], high word), filtered by `cur` = an earlier
+// (possibly stale, never too large) read of vtop[v].  Returns true if another edge deposited the
+// same 64-bit key: the returning atomicMax sees it, because an edge is only skipped when a
+// strictly larger high word is already present.
+__device__ __forceinline__ bool deposit_key(const RoundParams& P, uint32_t v, unsigned long long key,
+                                            uint32_t cur) {
+  const uint32_t hi = static_cast<uint32_t>(key >> 32);
+  if (cur > hi) return false;
+  const unsigned long long old = atomicMax(P.vkey + v, key);
+  atomicMax(P.vtop + v, hi);
+  return old == key;
+}
+
+__device__ __forceinline__ bool key_wins_at(const RoundParams& P, uint32_t v, unsigned long long key) {
+  if (__ldcg(P.vtop + v) != static_cast<uint32_t>(key >> 32)) return false;
+  return __ldcg(P.vkey + v) == key;
 }
 
 __device__ __forceinline__ double base_of(const RoundParams& P, uint32_t e) {
@@ -164,17 +217,6 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, uint32_t* s_warp) {
 #pragma unroll
   for (int w = 0; w < kWarpsPerBlock; ++w) s += s_warp[w];
   return s;
-}
-
-// vkey[v] = max(vkey[v], key) with tie detection.  A plain L2 load filters out edges that
-// already lost (the running maximum only grows), so only O(log deg) of a vertex's edges reach
-// the atomic unit.  Returns true if another edge deposited the same key (this
-// detection is complete for the key that ends up being the maximum).
-__device__ __forceinline__ bool vertex_max(unsigned long long* slot, unsigned long long key) {
-  const unsigned long long cur = __ldcg(slot);
-  if (cur > key) return false;
-  if (cur == key) return true;
-  return atomicMax(slot, key) == key;
 }
 
 struct WeightStats {
