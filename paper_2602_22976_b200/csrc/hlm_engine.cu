@@ -128,8 +128,9 @@ void Workspace::release() {
     dev_free(seg_ids[b]);
     dev_free(seg_cnt[b]);
     dev_free(list1[b]);
-    dev_free(mflag[b]);
   }
+  dev_free(cand_ids);
+  dev_free(cand_cnt);
   dev_free(matched_cnt);
   dev_free(deact_cnt);
   dev_free(va);
@@ -384,8 +385,8 @@ static int ensure_workspace(Graph* g, uint32_t max_rounds) {
       ST_CHECK(dev_alloc(&w.seg_cnt[b], w.nseg, g));
       ST_CHECK(dev_alloc(&w.list1[b], g->num_large, g));
     }
-    ST_CHECK(dev_alloc(&w.mflag[0], static_cast<size_t>(w.nseg) * w.seg_cap, g));
-    ST_CHECK(dev_alloc(&w.mflag[1], g->num_large, g));
+    ST_CHECK(dev_alloc(&w.cand_ids, static_cast<size_t>(w.nseg) * w.seg_cap, g));
+    ST_CHECK(dev_alloc(&w.cand_cnt, w.nseg, g));
     w.num_chunks = (w.mbits_words + kAsmChunkWords - 1) / kAsmChunkWords;
     ST_CHECK(dev_alloc(&w.chunk_cnt, w.num_chunks, g));
     ST_CHECK(dev_alloc(&w.scan_total, 1, g));
@@ -644,8 +645,8 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   }
   P.nseg = w.nseg;
   P.seg_cap = w.seg_cap;
-  P.mflag0 = w.mflag[0];
-  P.mflag1 = w.mflag[1];
+  P.cand_ids = w.cand_ids;
+  P.cand_cnt = w.cand_cnt;
   P.matched_cnt = w.matched_cnt;
   P.deact_cnt = w.deact_cnt;
 
@@ -835,6 +836,9 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   }
   CU_CHECK(cudaEventRecord(w.ev1, s));
   CU_CHECK(cudaStreamSynchronize(s));
+  // the device counts every edge dropped from the active list; the reference's "deactivated"
+  // excludes the ones that matched (local_max_par.hpp:166-168)
+  for (uint32_t q = 0; q < rounds; ++q) out->per_round_deactivated[q] -= out->per_round_matched[q];
   float ms = 0.f;
   CU_CHECK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   out->device_ms = ms;

@@ -40,7 +40,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
   const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
   uint32_t* __restrict__ out = P.seg_ids[par ^ 1];
   uint32_t* __restrict__ out_cnt = P.seg_cnt[par ^ 1];
-  const uint8_t* __restrict__ mflag = P.mflag0;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -56,20 +55,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
     if (seg >= P.nseg) continue;
     const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
     const uint32_t seg_base = seg * P.seg_cap;
-    uint32_t out_off = 0;
+    uint32_t out_off = 0, cand_off = 0;
     for (uint32_t t0 = 0; t0 < cnt; t0 += STEP) {
       uint32_t e[ITEMS];
-      bool survive[ITEMS];
+      bool survive[ITEMS], cand[ITEMS];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const uint32_t idx = t0 + k * 32 + lane;
-        survive[k] = false;
+        survive[k] = idx < cnt;
+        cand[k] = false;
         e[k] = 0;
-        if (idx < cnt) {
-          const uint32_t phys = seg_base + idx;
-          e[k] = in_ident ? phys : in[phys];
-          survive[k] = !(r > 1 && mflag[phys]);
-        }
+        if (survive[k]) e[k] = in_ident ? seg_base + idx : in[seg_base + idx];
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
@@ -111,8 +107,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
             if (survive[k]) {
               const unsigned long long key =
                   priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
+              const uint32_t hi = static_cast<uint32_t>(key >> 32);
+              bool lost = false;
 #pragma unroll
-              for (int i = 0; i < D; ++i) tie |= deposit_key(P, pv[k].v[i], key, cur[k][i]);
+              for (int i = 0; i < D; ++i) {
+                tie |= deposit_key(P, pv[k].v[i], key, cur[k][i]);
+                lost |= cur[k][i] > hi;  // a larger key was already there: cannot win this round
+              }
+              cand[k] = !lost;
             }
         }
       } else {
@@ -135,10 +137,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
               const unsigned long long key =
                   priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
               const bool peek = r > 1 || P.ks.precheck;
+              const uint32_t hi = static_cast<uint32_t>(key >> 32);
+              bool lost = false;
               for (uint32_t i = 0; i < s; ++i) {
                 const uint32_t v = __ldg(pp + i);
-                tie |= deposit_key(P, v, key, peek ? __ldcg(P.vtop + v) : 0u);
+                const uint32_t cur = peek ? __ldcg(P.vtop + v) : 0u;
+                tie |= deposit_key(P, v, key, cur);
+                lost |= cur > hi;
               }
+              cand[0] = !lost;
             }
           }
         }
@@ -152,10 +159,20 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
           out_off += __popc(ballot);
         }
       }
+      if constexpr (VMAX) {
+        // edges that may still win go to the (dense) candidate list of the check kernel
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t ballot = __ballot_sync(0xffffffffu, cand[k]);
+          if (cand[k]) P.cand_ids[seg_base + cand_off + __popc(ballot & lt_mask)] = e[k];
+          cand_off += __popc(ballot);
+        }
+      }
     }
     if (lane == 0) {
       const uint32_t kept = out_ident ? cnt : out_off;
       out_cnt[seg] = kept;
+      if (VMAX) P.cand_cnt[seg] = cand_off;
       local_kept += kept;
     }
   }
@@ -176,10 +193,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
   const uint32_t par = c->parity;
-  const bool ident = r == 1;
-  const uint32_t* __restrict__ list = P.seg_ids[par ^ 1];
-  const uint32_t* __restrict__ list_cnt = P.seg_cnt[par ^ 1];
-  uint8_t* __restrict__ mflag = P.mflag0;
+  const uint32_t* __restrict__ list = P.cand_ids;
+  const uint32_t* __restrict__ list_cnt = P.cand_cnt;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t local_matched = 0;
@@ -201,7 +216,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
         const uint32_t idx = t0 + k * 32 + lane;
         valid[k] = idx < cnt;
         win[k] = false;
-        e[k] = valid[k] ? (ident ? seg_base + idx : list[seg_base + idx]) : 0u;
+        e[k] = valid[k] ? list[seg_base + idx] : 0u;
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
@@ -271,9 +286,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
           }
         }
       }
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k)
-        if (valid[k]) mflag[seg_base + t0 + k * 32 + lane] = win[k] ? 1 : 0;
     }
   }
   const uint32_t t = block_sum(local_matched, s_warp);
@@ -291,7 +303,6 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   const uint32_t cnt = c->count1[par];
   const uint32_t* __restrict__ in = P.list1[par];
   uint32_t* __restrict__ out = P.list1[par ^ 1];
-  const uint8_t* __restrict__ mflag = P.mflag1;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -300,7 +311,6 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   bool tie = false;
   for (uint32_t pos = warp; pos < cnt; pos += nwarps) {
     const uint32_t e = in[pos];
-    if (r > 1 && mflag[pos]) continue;
     uint64_t b;
     uint32_t s;
     P.csr.range(e, b, s);
@@ -333,7 +343,6 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
   const uint32_t par = c->parity;
   const uint32_t cnt = c->count1[par ^ 1];
   const uint32_t* __restrict__ list = P.list1[par ^ 1];
-  uint8_t* __restrict__ mflag = P.mflag1;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -363,7 +372,6 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
         ++local_matched;
       }
     }
-    if (lane == 0) mflag[pos] = win ? 1 : 0;
   }
   if (local_matched) atomicAdd(P.matched_cnt + r, local_matched);
 }
@@ -427,7 +435,6 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
   const uint32_t r = X.round;
   const uint64_t slots = X.cls == 0 ? static_cast<uint64_t>(P.nseg) * P.seg_cap : X.count1;
-  uint8_t* mflag = X.cls == 0 ? P.mflag0 : P.mflag1;
   uint32_t local_matched = 0;
   for (uint64_t pos = warp; pos < slots; pos += nwarps) {
     uint32_t e;
@@ -443,7 +450,6 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
     uint32_t s;
     P.csr.range(e, b, s);
     if (X.cls == 0 && P.has_large && s > kLargeEdge) {
-      if (LEVEL == 4 && lane == 0) mflag[pos] = 0;
       continue;
     }
     const uint32_t* __restrict__ pp = P.csr.pins + b;
@@ -476,8 +482,7 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
           ++local_matched;
         }
       }
-      if (lane == 0) mflag[pos] = win ? 1 : 0;
-    }
+      }
   }
   if (LEVEL == 4 && local_matched) atomicAdd(P.matched_cnt + r, local_matched);
 }

@@ -99,12 +99,12 @@ struct RoundParams {
   uint32_t* seg_cnt[2];      // [buffer][nseg] ids in use per region
   uint32_t nseg;
   uint32_t seg_cap;
-  uint8_t* mflag0;           // per class-0 list slot: matched in the round just checked
+  uint32_t* cand_ids;        // class 0, same regions: edges that did not lose during vertex-max
+  uint32_t* cand_cnt;        // [nseg]
   // class 1: appended list
   uint32_t* list1[2];
-  uint8_t* mflag1;
   uint32_t* matched_cnt;     // [round] edges matched in that round
-  uint32_t* deact_cnt;       // [round] edges deactivated in that round
+  uint32_t* deact_cnt;       // [round] edges dropped after that round (matched + deactivated)
 };
 
 // vtop[v] mirrors the high 32 bits of vkey[v] (round tag + the leading payload bits).  It is half
