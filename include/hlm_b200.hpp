@@ -1,0 +1,176 @@
+// hlm_b200.hpp -- header-only C++ shim: the reference's matching API on top of the C-ABI.
+//
+// Include it AFTER the reference's headers ("hlm/hlm.hpp" or "hlm/local_max_par.hpp") and link
+// libhlm_b200.so.  It provides, in namespace hlm::b200, functions with the reference's own
+// signatures that fill real hlm::MatchResult objects and throw the reference's exception types:
+//
+//   hlm::MatchResult hlm::b200::run_variant(const Hypergraph&, const WeightStream&, const ParallelConfig&)
+//       replaces hlm::run_variant           (local_max_par.hpp:586)
+//   hlm::b200::local_max_crcw / local_max_crew
+//       replace hlm::local_max_crcw / local_max_crew (local_max_par.hpp:190,258)
+//   hlm::VerificationReport hlm::b200::verify_matching(const Hypergraph&, const Matching&)
+//       replaces hlm::verify_matching       (exact.hpp:115)
+//   class hlm::b200::ResidentHypergraph     -- upload once, match many times (bench protocol)
+//
+// Errors: HLM_B200_ERR_INPUT -> hlm::input_error; HLM_B200_ERR_ROUND_LIMIT ->
+// hlm::round_limit_error carrying the partial matching and report (matching.hpp:77-85);
+// anything else -> std::runtime_error.  ParallelConfig::workers / grain are ignored (the device
+// decides its own parallelism; results never depend on them, test_par.cpp:32-55).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hlm_b200.h"
+
+#ifndef HLM_B200_NO_REFERENCE_HEADERS
+#include "hlm/exact.hpp"
+#include "hlm/local_max_par.hpp"
+#endif
+
+namespace hlm {
+namespace b200 {
+
+namespace detail {
+
+inline hlm_b200_csr_view view_of(const Hypergraph& h) {
+  hlm_b200_csr_view v;
+  v.num_vertices = h.num_vertices;
+  v.num_edges = h.num_edges;
+  v.vertex_offsets = h.vertex_offsets.data();
+  v.vertex_incidence = h.vertex_incidence.data();
+  v.edge_offsets = h.edge_offsets.data();
+  v.edge_members = h.edge_members.data();
+  v.base_weights = h.base_weights.data();
+  return v;
+}
+
+inline hlm_b200_stream stream_of(const WeightStream& s) {
+  hlm_b200_stream c;
+  c.seed = s.seed;
+  c.kind = static_cast<int32_t>(s.kind);
+  c.mode = static_cast<int32_t>(s.mode);
+  c.noise_low = s.noise_low;
+  c.noise_high = s.noise_high;
+  return c;
+}
+
+inline hlm_b200_config config_of(const ParallelConfig& cfg) {
+  hlm_b200_config c;
+  c.variant = static_cast<int32_t>(cfg.variant);
+  c.max_rounds = cfg.max_rounds;
+  c.loop_mode = HLM_B200_LOOP_AUTO;
+  c.tie_mode = HLM_B200_TIES_AUTO;
+  c.flags = 0;
+  return c;
+}
+
+// hlm_b200_result -> hlm::MatchResult (matching.hpp:15-48); frees the C result.
+inline MatchResult take(hlm_b200_result& r) {
+  MatchResult out;
+  Matching& m = out.matching;
+  RunReport& rep = out.report;
+  m.matched_edges.assign(r.matched_edges, r.matched_edges + r.num_matched);
+  m.total_weight = r.total_weight;
+  m.rounds_used = r.rounds;
+  m.per_round_matched.assign(r.per_round_matched, r.per_round_matched + r.rounds);
+  rep.rounds = r.rounds;
+  rep.matched_per_round_count = m.per_round_matched;
+  rep.deactivated_per_round.assign(r.per_round_deactivated, r.per_round_deactivated + r.rounds);
+  rep.matched_per_round.assign(r.rounds, {});
+  for (std::uint32_t q = 0; q < r.rounds; ++q) rep.matched_per_round[q].reserve(m.per_round_matched[q]);
+  if (r.matched_round)
+    for (std::uint64_t i = 0; i < r.num_matched; ++i)  // ids ascend, so every per-round list does too
+      rep.matched_per_round[r.matched_round[i] - 1].push_back(r.matched_edges[i]);
+  rep.work.rounds = r.rounds;
+  rep.work.total_edge_visits = r.total_edge_visits;
+  rep.work.total_pin_visits = r.total_pin_visits;
+  rep.wall_time_ms = r.wall_time_ms;
+  rep.write_conflicts = r.write_conflicts;
+  hlm_b200_result_free(&r);
+  return out;
+}
+
+inline MatchResult finish(int status, hlm_b200_result& r) {
+  if (status == HLM_B200_OK) return take(r);
+  if (status == HLM_B200_ERR_ROUND_LIMIT) {
+    MatchResult partial = take(r);
+    throw round_limit_error(std::move(partial.matching), std::move(partial.report));
+  }
+  const std::string msg = hlm_b200_last_error();
+  hlm_b200_result_free(&r);
+  if (status == HLM_B200_ERR_INPUT) throw input_error(msg);
+  throw std::runtime_error("hlm_b200: " + msg);
+}
+
+}  // namespace detail
+
+// run_variant (local_max_par.hpp:586): upload + match + release in one synchronous call.
+inline MatchResult run_variant(const Hypergraph& h, const WeightStream& stream, const ParallelConfig& cfg,
+                               int device = 0) {
+  const hlm_b200_csr_view v = detail::view_of(h);
+  const hlm_b200_stream s = detail::stream_of(stream);
+  const hlm_b200_config c = detail::config_of(cfg);
+  hlm_b200_result r;
+  const int st = hlm_b200_match_host(&v, &s, &c, device, &r);
+  return detail::finish(st, r);
+}
+
+inline MatchResult local_max_crcw(const Hypergraph& h, const WeightStream& stream, ParallelConfig cfg = {}) {
+  cfg.variant = Variant::crcw;
+  return ::hlm::b200::run_variant(h, stream, cfg, 0);
+}
+
+inline MatchResult local_max_crew(const Hypergraph& h, const WeightStream& stream, ParallelConfig cfg = {}) {
+  cfg.variant = Variant::crew;
+  return ::hlm::b200::run_variant(h, stream, cfg, 0);
+}
+
+// An instance resident in HBM: the loader's output.  Matching it repeatedly excludes the
+// host-to-device copy, which is the paper's timing protocol.
+class ResidentHypergraph {
+ public:
+  explicit ResidentHypergraph(const Hypergraph& h, int device = 0) {
+    const hlm_b200_csr_view v = detail::view_of(h);
+    const int st = hlm_b200_graph_upload(&v, device, &g_);
+    if (st == HLM_B200_ERR_INPUT) throw input_error(hlm_b200_last_error());
+    if (st != HLM_B200_OK) throw std::runtime_error(std::string("hlm_b200: ") + hlm_b200_last_error());
+  }
+  ResidentHypergraph(const ResidentHypergraph&) = delete;
+  ResidentHypergraph& operator=(const ResidentHypergraph&) = delete;
+  ~ResidentHypergraph() { hlm_b200_graph_release(g_); }
+
+  MatchResult run_variant(const WeightStream& stream, const ParallelConfig& cfg) const {
+    const hlm_b200_stream s = detail::stream_of(stream);
+    const hlm_b200_config c = detail::config_of(cfg);
+    hlm_b200_result r;
+    const int st = hlm_b200_match(g_, &s, &c, &r);
+    return detail::finish(st, r);
+  }
+
+  VerificationReport verify_matching(const Matching& m) const {
+    int disjoint = 0, maximal = 0;
+    double weight = 0.0;
+    const int st = hlm_b200_verify(g_, m.matched_edges.data(), m.matched_edges.size(), &disjoint, &maximal, &weight);
+    if (st == HLM_B200_ERR_INPUT) throw input_error(hlm_b200_last_error());  // exact.hpp:117
+    if (st != HLM_B200_OK) throw std::runtime_error(std::string("hlm_b200: ") + hlm_b200_last_error());
+    VerificationReport rep;
+    rep.disjoint = disjoint != 0;
+    rep.maximal = maximal != 0;
+    rep.weight = weight;
+    return rep;
+  }
+
+ private:
+  hlm_b200_graph* g_ = nullptr;
+};
+
+inline VerificationReport verify_matching(const Hypergraph& h, const Matching& m, int device = 0) {
+  return ResidentHypergraph(h, device).verify_matching(m);
+}
+
+}  // namespace b200
+}  // namespace hlm

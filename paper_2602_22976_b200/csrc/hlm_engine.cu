@@ -363,7 +363,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out) {
 // ---------------------------------------------------------------------------------------------
 // workspace + key scheme
 // ---------------------------------------------------------------------------------------------
-static int ensure_workspace(Graph* g, uint32_t max_rounds) {
+int ensure_workspace(Graph* g, uint32_t max_rounds) {
   Workspace& w = g->ws;
   if (!w.ctrl) {
     ST_CHECK(dev_alloc(&w.ctrl, 1, g));

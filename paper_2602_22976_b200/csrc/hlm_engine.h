@@ -105,6 +105,7 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins);
 int finish_weights(Graph* g);
 int weight_stats(Graph* g, double lo, WeightStats* out);
 int build_incidence(Graph* g);
+int ensure_workspace(Graph* g, uint32_t max_rounds);
 bool reorder_enabled();
 int reorder_by_first_pin(Graph* g);
 int download_pins_original_order(Graph* g, uint32_t* host_pins);
