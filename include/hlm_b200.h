@@ -178,6 +178,45 @@ int hlm_b200_verify(hlm_b200_graph* g, const uint32_t* matched, uint64_t count, 
 int hlm_b200_eval_stream(const hlm_b200_stream* stream, const uint32_t* edges, const uint32_t* rounds,
                          const double* base, size_t count, double* w_out, uint64_t* t_out, int device);
 
+/* ---- edge-partitioned (multi-GPU) runs -----------------------------------------------------
+ * No reference counterpart (the reference is single-process; PAPER.md:418 only sketches it).
+ * One process per GPU holds the edge rows [edge_begin, edge_begin + m_local) of the instance
+ * (hlm_b200_syn_spec, or an uploaded shard) and the replicated per-vertex arrays.  The caller
+ * owns the two device arrays that cross ranks and all-reduces them between the steps
+ * (paper_2602_22976_b200/multi_gpu.py does it with torch.distributed / NCCL); the protocol is
+ * documented at the top of csrc/hlm_multi.inc.  Results are identical for every rank count. */
+typedef struct {
+  double base_min;      /* of the local base weights */
+  double base_max;
+  int32_t non_integer;  /* some fl(base + noise_low) is not an integer below 2^32 */
+  uint32_t num_edges;
+} hlm_b200_weight_info;
+
+typedef struct {
+  void* vkey;                 /* device, uint64[num_vertices]: all-reduce(max) as int64 */
+  void* exch;                 /* device, int32[hlm_b200_mg_exch_words(n)]: all-reduce(sum) */
+  double base_min;            /* GLOBAL weight facts (reduce hlm_b200_graph_weight_info over ranks) */
+  double base_max;
+  int32_t non_integer;
+  uint32_t num_edges_global;  /* for default_max_rounds */
+} hlm_b200_mg_setup;
+
+enum { HLM_B200_MG_RUNNING = 0, HLM_B200_MG_DONE = 1, HLM_B200_MG_ROUND_LIMIT = 2 };
+
+uint64_t hlm_b200_mg_exch_words(uint32_t num_vertices);
+int hlm_b200_graph_weight_info(hlm_b200_graph* g, double noise_low, hlm_b200_weight_info* info);
+int hlm_b200_mg_begin(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
+                      const hlm_b200_mg_setup* setup);
+int hlm_b200_mg_vertex_max(hlm_b200_graph* g);
+int hlm_b200_mg_claims(hlm_b200_graph* g);
+int hlm_b200_mg_decide(hlm_b200_graph* g, uint32_t* global_active, int* tie);
+int hlm_b200_mg_check_commit(hlm_b200_graph* g);
+int hlm_b200_mg_exact_level(hlm_b200_graph* g, int level, void* va, void* vb, void* vc);
+int hlm_b200_mg_end_round(hlm_b200_graph* g, uint32_t global_active, int* status);
+/* weight_before: total_weight of the shards with lower edge ids (the reference sums base weights
+ * in ascending-id order, local_max_seq.hpp:79; FP64 addition is not associative). */
+int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result* out);
+
 /* default_max_rounds (matching.hpp:87-89). */
 uint32_t hlm_b200_default_max_rounds(uint32_t num_edges);
 

@@ -53,6 +53,16 @@ class SynSpec(C.Structure):
                 ("edge_begin", C.c_uint32), ("m_local", C.c_uint32)]
 
 
+class WeightInfo(C.Structure):
+    _fields_ = [("base_min", C.c_double), ("base_max", C.c_double), ("non_integer", C.c_int32),
+                ("num_edges", C.c_uint32)]
+
+
+class MgSetup(C.Structure):
+    _fields_ = [("vkey", C.c_void_p), ("exch", C.c_void_p), ("base_min", C.c_double), ("base_max", C.c_double),
+                ("non_integer", C.c_int32), ("num_edges_global", C.c_uint32)]
+
+
 # every symbol include/hlm_b200.h declares: (restype, argtypes)
 SYMBOLS = {
     "hlm_b200_abi_version": (C.c_int, []),
@@ -73,6 +83,16 @@ SYMBOLS = {
     "hlm_b200_eval_stream": (C.c_int, [C.POINTER(Stream), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                        C.c_void_p, C.c_void_p, C.c_int]),
     "hlm_b200_default_max_rounds": (C.c_uint32, [C.c_uint32]),
+    "hlm_b200_mg_exch_words": (C.c_uint64, [C.c_uint32]),
+    "hlm_b200_graph_weight_info": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(WeightInfo)]),
+    "hlm_b200_mg_begin": (C.c_int, [C.c_void_p, C.POINTER(Stream), C.POINTER(Config), C.POINTER(MgSetup)]),
+    "hlm_b200_mg_vertex_max": (C.c_int, [C.c_void_p]),
+    "hlm_b200_mg_claims": (C.c_int, [C.c_void_p]),
+    "hlm_b200_mg_decide": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
+    "hlm_b200_mg_check_commit": (C.c_int, [C.c_void_p]),
+    "hlm_b200_mg_exact_level": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hlm_b200_mg_end_round": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_int)]),
+    "hlm_b200_mg_finish": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(Result)]),
 }
 
 _lib = None

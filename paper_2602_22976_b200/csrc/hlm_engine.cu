@@ -152,8 +152,11 @@ void Workspace::release() {
   *this = Workspace();
 }
 
+static void mg_release(Graph* g);
+
 Graph::~Graph() {
   cudaSetDevice(device);
+  mg_release(this);
   ws.release();
   crew_release(this);
   dev_free(pins);
@@ -420,8 +423,20 @@ static int ensure_exact_arrays(Graph* g) {
 }
 
 // Picks the 64-bit key layout for this (instance, stream) pair; see hlm_priority.cuh.
-static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_rounds, KeyScheme* ks) {
+// Weight facts of the WHOLE instance (edge shards agree on them before choosing a key layout).
+struct WeightBounds {
+  double base_min, base_max;
+  bool constant;     // every base weight equal
+  bool non_integer;  // some fl(base + lo) is not an integer below 2^32
+};
+
+static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_rounds, KeyScheme* ks,
+                             const WeightBounds* global = nullptr, bool signed_safe = false) {
   std::memset(ks, 0, sizeof(*ks));
+  const int width_bits = signed_safe ? 63 : 64;  // keep bit 63 clear when keys travel as int64
+  const double bmin = global ? global->base_min : g->base_min;
+  const double bmax = global ? global->base_max : g->base_max;
+  const bool constant = global ? global->constant : g->base == nullptr;
   double wmin, wmax;
   bool int_hash = false;
   uint64_t wq_min = 0, wq_span = 0;
@@ -429,17 +444,21 @@ static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_roun
     wmin = 0x1.0p-54;  // to_unit_interval_64(0) (weight_stream.hpp:49-52); park-miller >= 1/(2^31-1)
     wmax = 1.0;
   } else if (sp.width != 0.0) {
-    wmin = g->base_min + sp.lo;
-    wmax = (g->base_max + sp.lo) + sp.width;  // u < 1 and rounding is monotone
+    wmin = bmin + sp.lo;
+    wmax = (bmax + sp.lo) + sp.width;  // u < 1 and rounding is monotone
   } else {
-    wmin = g->base_min + sp.lo;
-    wmax = g->base_max + sp.lo;
-    if (!g->base) {
+    wmin = bmin + sp.lo;
+    wmax = bmax + sp.lo;
+    if (constant) {
       int_hash = true;  // every edge has the same weight: order is (tie_hash, id)
       wq_min = static_cast<uint64_t>(wmin);
     } else {
       WeightStats ws;
-      ST_CHECK(weight_stats(g, sp.lo, &ws));
+      if (global) {
+        ws.non_integer = global->non_integer;
+      } else {
+        ST_CHECK(weight_stats(g, sp.lo, &ws));
+      }
       if (!ws.non_integer && wmax - wmin < 65536.0) {
         int_hash = true;
         wq_min = static_cast<uint64_t>(wmin);
@@ -452,7 +471,7 @@ static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_roun
     int tag_bits = std::max(8, bitlen64(max_rounds));
     if (tag_bits > 16) tag_bits = 16;
     ks->kind = KEY_INT_HASH;
-    ks->payload_bits = 64 - tag_bits;
+    ks->payload_bits = width_bits - tag_bits;
     ks->hash_bits = ks->payload_bits - qb;
     ks->wq_min = wq_min;
     ks->tag_period = (1u << tag_bits) - 2u;  // the all-ones tag is kVertexDead
@@ -462,7 +481,7 @@ static int choose_key_scheme(Graph* g, const StreamParams& sp, uint32_t max_roun
   ks->kind = KEY_WEIGHT_BITS;
   ks->payload_bits = std::max(1, bitlen64(span));
   ks->wmin_bits = dbits(wmin);
-  const int tag_bits = 64 - ks->payload_bits;
+  const int tag_bits = width_bits - ks->payload_bits;
   ks->tag_period = tag_bits >= 16 ? 65534u : (tag_bits >= 2 ? (1u << tag_bits) - 2u : 0u);  // 0: no fast path
   return HLM_B200_OK;
 }
@@ -505,8 +524,8 @@ struct Launcher {
       ++launches;
     }
   }
-  void advance(cudaStream_t s, cudaGraphConditionalHandle h, int in_graph) {
-    k_advance<<<1, 1, 0, s>>>(P, h, in_graph);
+  void advance(cudaStream_t s, cudaGraphConditionalHandle h, int in_graph, uint32_t active_elsewhere = 0) {
+    k_advance<<<1, 1, 0, s>>>(P, h, in_graph, active_elsewhere);
     ++launches;
   }
 };
@@ -595,17 +614,10 @@ static bool same_params(const RoundParams& a, const RoundParams& b) {
   return std::memcmp(&a, &b, sizeof(RoundParams)) == 0;
 }
 
-int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
-  const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
-  if (max_rounds > 65000u) {
-    set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
-    return HLM_B200_ERR_UNSUPPORTED;
-  }
-  cudaStream_t s = g->stream;
-  ST_CHECK(ensure_workspace(g, max_rounds));
+// Fills the kernel parameter block for one matching of `g` under stream `st`.
+static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, uint32_t max_rounds,
+                          Launcher& L, const WeightBounds* global, bool signed_safe) {
   Workspace& w = g->ws;
-
-  Launcher L;
   L.g = g;
   L.exact = cfg->tie_mode == HLM_B200_TIES_EXACT;
   RoundParams& P = L.P;
@@ -624,7 +636,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   P.stream.lo = st->noise_low;
   P.stream.hi = st->noise_high;
   P.stream.width = st->noise_high - st->noise_low;
-  ST_CHECK(choose_key_scheme(g, P.stream, max_rounds, &P.ks));
+  ST_CHECK(choose_key_scheme(g, P.stream, max_rounds, &P.ks, global, signed_safe));
   if (P.ks.tag_period == 0) {  // weights span too many binades for a tagged 64-bit key
     L.exact = true;
     P.ks.tag_period = 65534u;
@@ -656,6 +668,23 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     g->round_grid = g->num_sms * std::max(1, occ);
     g->large_grid = g->num_sms * 4;
   }
+
+  return HLM_B200_OK;
+}
+
+int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+  const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
+  if (max_rounds > 65000u) {
+    set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
+    return HLM_B200_ERR_UNSUPPORTED;
+  }
+  cudaStream_t s = g->stream;
+  ST_CHECK(ensure_workspace(g, max_rounds));
+  Workspace& w = g->ws;
+
+  Launcher L;
+  ST_CHECK(setup_launcher(g, st, cfg, max_rounds, L, nullptr, false));
+  RoundParams& P = L.P;
 
   bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact;
   if (use_graph && (!w.graph_exec || !same_params(w.graph_key, P))) ST_CHECK(build_loop_graph(L));
@@ -776,7 +805,7 @@ static int ensure_pinned(Workspace& w, uint64_t total, bool need_w) {
 // finish_matching (local_max_seq.hpp:74-83) + the RunReport counters.  Expects the matched
 // bitmap (ws.mbits) and the per-edge round record (ws.mround) to be final.
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
-                    hlm_b200_result* out) {
+                    hlm_b200_result* out, double weight_before) {
   Workspace& w = g->ws;
   cudaStream_t s = g->stream;
   const uint32_t m = g->m;
@@ -847,16 +876,18 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     if (want_round) std::memcpy(out->matched_round, w.pin_round, total * 2);
   }
   // total_weight accumulates base weights in ascending-id order (local_max_seq.hpp:79)
-  double tw = 0.0;
+  // (weight_before: the ordered sum over the lower-id shards of an edge-partitioned run)
+  double tw = weight_before;
   if (need_w) {
     const double* wts = static_cast<const double*>(w.pin_w);
     for (uint64_t i = 0; i < total; ++i) tw += wts[i];
   } else if (int_sum) {
-    tw = static_cast<double>(isum);
+    tw += static_cast<double>(isum);
   } else {
     const double b = g->base_const;
-    if (b == std::floor(b) && b * static_cast<double>(total) < 9007199254740992.0) {
-      tw = b * static_cast<double>(total);  // exact: every partial sum is an integer below 2^53
+    if (b == std::floor(b) && weight_before == std::floor(weight_before) &&
+        weight_before + b * static_cast<double>(total) < 9007199254740992.0) {
+      tw += b * static_cast<double>(total);  // exact: every partial sum is an integer below 2^53
     } else {
       for (uint64_t i = 0; i < total; ++i) tw += b;
     }
@@ -911,6 +942,8 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return rc;
 }
+
+#include "hlm_multi.inc"
 
 // ---------------------------------------------------------------------------------------------
 // verify_matching (exact.hpp:115-140)
@@ -1065,6 +1098,50 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   rc = run_match(g, stream, cfg, out);
   delete g;
   return rc;
+}
+
+uint64_t hlm_b200_mg_exch_words(uint32_t num_vertices) { return mg_exch_words(num_vertices); }
+
+int hlm_b200_graph_weight_info(hlm_b200_graph* gh, double noise_low, hlm_b200_weight_info* info) {
+  if (!gh || !info) return HLM_B200_ERR_INPUT;
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  CU_CHECK(cudaSetDevice(g->device));
+  info->base_min = g->base_min;
+  info->base_max = g->base_max;
+  if (g->base && g->m) {
+    WeightStats ws;
+    ST_CHECK(weight_stats(g, noise_low, &ws));
+    info->non_integer = ws.non_integer ? 1 : 0;
+  } else {
+    const double w = g->base_const + noise_low;
+    info->non_integer = (w == std::floor(w) && w < 4294967296.0) ? 0 : 1;
+  }
+  info->num_edges = g->m;
+  return HLM_B200_OK;
+}
+
+int hlm_b200_mg_begin(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
+                      const hlm_b200_mg_setup* setup) {
+  if (!g || !stream || !cfg) return HLM_B200_ERR_INPUT;
+  return mg_begin(reinterpret_cast<Graph*>(g), stream, cfg, setup);
+}
+int hlm_b200_mg_vertex_max(hlm_b200_graph* g) { return mg_vertex_max(reinterpret_cast<Graph*>(g)); }
+int hlm_b200_mg_claims(hlm_b200_graph* g) { return mg_claims(reinterpret_cast<Graph*>(g)); }
+int hlm_b200_mg_decide(hlm_b200_graph* g, uint32_t* global_active, int* tie) {
+  if (!global_active || !tie) return HLM_B200_ERR_INPUT;
+  return mg_decide(reinterpret_cast<Graph*>(g), global_active, tie);
+}
+int hlm_b200_mg_check_commit(hlm_b200_graph* g) { return mg_check_commit(reinterpret_cast<Graph*>(g)); }
+int hlm_b200_mg_exact_level(hlm_b200_graph* g, int level, void* va, void* vb, void* vc) {
+  return mg_exact_level(reinterpret_cast<Graph*>(g), level, va, vb, vc);
+}
+int hlm_b200_mg_end_round(hlm_b200_graph* g, uint32_t global_active, int* status) {
+  if (!status) return HLM_B200_ERR_INPUT;
+  return mg_end_round(reinterpret_cast<Graph*>(g), global_active, status);
+}
+int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result* out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  return mg_finish(reinterpret_cast<Graph*>(g), weight_before, out);
 }
 
 void hlm_b200_result_free(hlm_b200_result* r) {

@@ -88,6 +88,7 @@ struct Graph {
   int round_grid = 0, large_grid = 0;
   Workspace ws;
   CrewState* crew = nullptr;
+  void* mg = nullptr;  // MgState of an edge-partitioned run in progress (hlm_multi.inc)
   EdgeCsr csr() const;
   ~Graph();
 };
@@ -114,7 +115,7 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);
 void crew_release(Graph* g);
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
-                    hlm_b200_result* out);
+                    hlm_b200_result* out, double weight_before = 0.0);
 int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out, uint64_t count,
                                      uint64_t* total);
 
