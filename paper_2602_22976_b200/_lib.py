@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhlm_b200.so")
+LIB_PATH = os.environ.get("HLM_B200_LIB") or os.path.join(_HERE, "lib", "libhlm_b200.so")
 
 OK, ERR_INPUT, ERR_ROUND_LIMIT, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = range(6)
 

@@ -664,11 +664,10 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
 
   if (!g->round_grid) {
     int occ = 0;
-    CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_vmax_small<4, true>, kBlock, 0));
+    CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_vmax_small<2, true>, kBlock, 0));
     g->round_grid = g->num_sms * std::max(1, occ);
     g->large_grid = g->num_sms * 4;
   }
-
   return HLM_B200_OK;
 }
 

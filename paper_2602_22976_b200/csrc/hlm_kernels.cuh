@@ -10,9 +10,22 @@ namespace hlmb {
 // Round kernels, class 0: one thread per edge (size <= kLargeEdge), ITEMS edges per thread and
 // tile.  D > 0: uniform edge size, one 64/128-bit pin load per edge; D == 0: runtime offsets.
 // ---------------------------------------------------------------------------------------------
+#ifndef HLM_ITEMS_D2
+#define HLM_ITEMS_D2 1
+#endif
+#ifndef HLM_ITEMS_D4
+#define HLM_ITEMS_D4 1
+#endif
+#ifndef HLM_VTOP_LD
+#define HLM_VTOP_LD __ldca  // L1 may serve hub vertices: stale values are only ever too small (safe)
+#endif
+#ifndef HLM_MIN_BLOCKS
+#define HLM_MIN_BLOCKS 8
+#endif
+
 template <int D>
 struct TileShape {
-  static constexpr int kItems = (D == 2 || D == 4) ? 2 : 1;  // edges per lane and step
+  static constexpr int kItems = D == 2 ? HLM_ITEMS_D2 : (D == 4 ? HLM_ITEMS_D4 : 1);  // edges per lane and step
   static constexpr uint32_t kStep = 32 * kItems;             // edges per warp and step
 };
 
@@ -26,7 +39,7 @@ __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool iden
 // A CTA claims kWarpsPerBlock consecutive regions by ticket; each warp then owns one region and
 // runs on its own (ballot / popc compaction, no block barrier inside the sweep).
 template <int D, bool VMAX>
-__global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(const RoundParams P) {
   constexpr int ITEMS = TileShape<D>::kItems;
   constexpr uint32_t STEP = TileShape<D>::kStep;
   __shared__ uint32_t s_warp[kWarpsPerBlock];
@@ -87,7 +100,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
           for (int k = 0; k < ITEMS; ++k)
             if (survive[k]) {
 #pragma unroll
-              for (int i = 0; i < D; ++i) cur[k][i] = __ldcg(P.vtop + pv[k].v[i]);
+              for (int i = 0; i < D; ++i) cur[k][i] = HLM_VTOP_LD(P.vtop + pv[k].v[i]);
             }
 #pragma unroll
           for (int k = 0; k < ITEMS; ++k) {
@@ -184,7 +197,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_filter_vmax_small(const RoundPara
 }
 
 template <int D>
-__global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_check_commit_small(const RoundParams P) {
   constexpr int ITEMS = TileShape<D>::kItems;
   constexpr uint32_t STEP = TileShape<D>::kStep;
   __shared__ uint32_t s_warp[kWarpsPerBlock];
