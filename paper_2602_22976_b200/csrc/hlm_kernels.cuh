@@ -132,6 +132,9 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
         }
       } else {
         // runtime sizes: ITEMS == 1
+        bool is_long = false;
+        uint64_t long_b = 0;
+        uint32_t long_s = 0;
         if (survive[0]) {
           uint64_t b;
           uint32_t s;
@@ -140,24 +143,68 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
             survive[0] = false;  // class-1 edge seen through the identity list
           } else {
             const uint32_t* __restrict__ pp = P.csr.pins + b;
-            bool dead_any = false;
-            if (r > 1)
-              for (uint32_t i = 0; i < s; ++i) dead_any |= (__ldcg(P.vtop + __ldg(pp + i)) == kTopDead);
+            const bool peek = r > 1 || P.ks.precheck;
+            if (s <= 8) {
+              // short edge: every pin and its filter word in flight at once, one gather per pin
+              uint32_t v[8], cur[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = static_cast<uint32_t>(i) < s ? __ldg(pp + i) : 0u;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                cur[i] = (peek && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
+              bool dead_any = false;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
+              if (dead_any) {
+                survive[0] = false;
+                ++local_deact;
+              } else if constexpr (VMAX) {
+                const unsigned long long key =
+                    priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
+                const uint32_t hi = static_cast<uint32_t>(key >> 32);
+                bool lost = false;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  if (static_cast<uint32_t>(i) < s) {
+                    tie |= deposit_key(P, v[i], key, cur[i]);
+                    lost |= cur[i] > hi;
+                  }
+                cand[0] = !lost;
+              }
+            } else {
+              is_long = true;  // 9..32 pins: handled below by the whole warp, one pin per lane
+              long_b = b;
+              long_s = s;
+            }
+          }
+        }
+        // medium edges, one at a time, cooperatively: the 32 lanes take one pin each, so an edge
+        // costs one gather round trip instead of one per pin
+        uint32_t long_mask = __ballot_sync(0xffffffffu, is_long);
+        while (long_mask) {
+          const int src = __ffs(long_mask) - 1;
+          long_mask &= long_mask - 1;
+          const uint64_t eb = __shfl_sync(0xffffffffu, long_b, src);
+          const uint32_t es = __shfl_sync(0xffffffffu, long_s, src);
+          const uint32_t ee = __shfl_sync(0xffffffffu, e[0], src);
+          const bool mine = lane < es;
+          const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
+          const bool peek = r > 1 || P.ks.precheck;
+          const uint32_t cur = (mine && peek) ? HLM_VTOP_LD(P.vtop + v) : 0u;
+          const bool dead_any = __any_sync(0xffffffffu, mine && cur == kTopDead);
+          bool lost = false;
+          if (!dead_any) {
+            if constexpr (VMAX) {
+              const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, ee), r, base_of(P, ee), tag);
+              if (mine) tie |= deposit_key(P, v, key, cur);
+              lost = __any_sync(0xffffffffu, mine && cur > static_cast<uint32_t>(key >> 32));
+            }
+          }
+          if (static_cast<int>(lane) == src) {
             if (dead_any) {
               survive[0] = false;
               ++local_deact;
-            } else if constexpr (VMAX) {
-              const unsigned long long key =
-                  priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
-              const bool peek = r > 1 || P.ks.precheck;
-              const uint32_t hi = static_cast<uint32_t>(key >> 32);
-              bool lost = false;
-              for (uint32_t i = 0; i < s; ++i) {
-                const uint32_t v = __ldg(pp + i);
-                const uint32_t cur = peek ? __ldcg(P.vtop + v) : 0u;
-                tie |= deposit_key(P, v, key, cur);
-                lost |= cur > hi;
-              }
+            } else if (VMAX) {
               cand[0] = !lost;
             }
           }
