@@ -145,11 +145,19 @@ void Workspace::release() {
   if (pin_ids) cudaFreeHost(pin_ids);
   if (pin_round) cudaFreeHost(pin_round);
   if (pin_w) cudaFreeHost(pin_w);
-  if (graph_exec) cudaGraphExecDestroy(graph_exec);
-  if (graph) cudaGraphDestroy(graph);
+  drop_graphs();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   *this = Workspace();
+}
+
+void Workspace::drop_graphs() {
+  for (int k = 0; k < 2; ++k) {
+    if (graph_exec[k]) cudaGraphExecDestroy(graph_exec[k]);
+    if (graph[k]) cudaGraphDestroy(graph[k]);
+    graph_exec[k] = nullptr;
+    graph[k] = nullptr;
+  }
 }
 
 static void mg_release(Graph* g);
@@ -403,12 +411,7 @@ int ensure_workspace(Graph* g, uint32_t max_rounds) {
     w.rounds_cap = max_rounds + 3;
     ST_CHECK(dev_alloc(&w.matched_cnt, w.rounds_cap, g));
     ST_CHECK(dev_alloc(&w.deact_cnt, w.rounds_cap, g));
-    if (w.graph_exec) {  // captured kernel arguments point at the old arrays
-      cudaGraphExecDestroy(w.graph_exec);
-      cudaGraphDestroy(w.graph);
-      w.graph_exec = nullptr;
-      w.graph = nullptr;
-    }
+    w.drop_graphs();  // captured kernel arguments point at the old arrays
   }
   return HLM_B200_OK;
 }
@@ -495,14 +498,32 @@ struct Launcher {
   bool exact;  // TIES_EXACT: no 64-bit keys at all
   uint32_t launches = 0;
 
+  // first_round: the launch is known to process round 1 (identity lists, nothing dead yet) and
+  // may use the specialised kernel; the general kernels are correct for every round.
   template <bool VMAX>
-  void filter(cudaStream_t s) {
-    const int grid = g->round_grid;
-    switch (g->uniform_d) {
-      case 2: k_filter_vmax_small<2, VMAX><<<grid, kBlock, 0, s>>>(P); break;
-      case 4: k_filter_vmax_small<4, VMAX><<<grid, kBlock, 0, s>>>(P); break;
-      case 8: k_filter_vmax_small<8, VMAX><<<grid, kBlock, 0, s>>>(P); break;
-      default: k_filter_vmax_small<0, VMAX><<<grid, kBlock, 0, s>>>(P); break;
+  void filter(cudaStream_t s, bool first_round = false) {
+    const int grid = g->sweep_grid;
+#ifdef HLM_SIMPLE_R1
+    if (false) {
+#else
+    if (VMAX && first_round) {
+#endif
+      switch (g->uniform_d) {
+        case 2: k_sweep_uniform<2, true, true><<<grid, kBlock, 0, s>>>(P); break;
+        case 4: k_sweep_uniform<4, true, true><<<grid, kBlock, 0, s>>>(P); break;
+        case 8: k_sweep_uniform<8, true, true><<<grid, kBlock, 0, s>>>(P); break;
+        default: k_filter_vmax_small<true><<<grid, kBlock, 0, s>>>(P); break;
+      }
+    } else {
+      // later rounds, d = 2, 4: the occupancy-driven sweep wins; d = 8: the pipelined one
+      // (measured, profiles/README.md)
+      const int sgrid = g->num_sms * 8;
+      switch (g->uniform_d) {
+        case 2: k_sweep_uniform_simple<2, VMAX><<<sgrid, kBlock, 0, s>>>(P); break;
+        case 4: k_sweep_uniform_simple<4, VMAX><<<sgrid, kBlock, 0, s>>>(P); break;
+        case 8: k_sweep_uniform<8, VMAX, false><<<grid, kBlock, 0, s>>>(P); break;
+        default: k_filter_vmax_small<VMAX><<<g->round_grid, kBlock, 0, s>>>(P); break;
+      }
     }
     ++launches;
     if (g->num_large) {
@@ -511,7 +532,7 @@ struct Launcher {
     }
   }
   void check(cudaStream_t s) {
-    const int grid = g->round_grid;
+    const int grid = g->check_grid;
     switch (g->uniform_d) {
       case 2: k_check_commit_small<2><<<grid, kBlock, 0, s>>>(P); break;
       case 4: k_check_commit_small<4><<<grid, kBlock, 0, s>>>(P); break;
@@ -568,29 +589,53 @@ static int exact_round(Launcher& L, uint32_t r, uint32_t buf, const Ctrl& c) {
   return HLM_B200_OK;
 }
 
-static int build_loop_graph(Launcher& L) {
+// which = 0: [round 1: sweep (specialised kernel), check, advance] -> WHILE { sweep, check, advance }
+// which = 1: WHILE { sweep, check, advance } alone (resumes a run at any round)
+static int build_loop_graph(Launcher& L, int which) {
   Graph* g = L.g;
   Workspace& w = g->ws;
-  if (w.graph_exec) {
-    cudaGraphExecDestroy(w.graph_exec);
-    cudaGraphDestroy(w.graph);
-    w.graph_exec = nullptr;
-    w.graph = nullptr;
-  }
-  CU_CHECK(cudaGraphCreate(&w.graph, 0));
+  cudaGraph_t& graph = w.graph[which];
+  CU_CHECK(cudaGraphCreate(&graph, 0));
   cudaGraphConditionalHandle handle;
-  CU_CHECK(cudaGraphConditionalHandleCreate(&handle, w.graph, 1, cudaGraphCondAssignDefault));
+  CU_CHECK(cudaGraphConditionalHandleCreate(&handle, graph, which == 0 ? 0u : 1u, cudaGraphCondAssignDefault));
+  cudaStream_t cs;
+  CU_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraphNode_t last = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (which == 0) {
+    e = cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      const uint32_t before = L.launches;
+      L.filter<true>(cs, /*first_round=*/true);
+      L.check(cs);
+      L.advance(cs, handle, 1);
+      w.graph_head_launches = L.launches - before;
+      L.launches = before;
+      cudaStreamCaptureStatus st;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      e = cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &ndeps);
+      if (e == cudaSuccess && ndeps == 1) last = deps[0];
+      cudaGraph_t same = nullptr;
+      const cudaError_t e2 = cudaStreamEndCapture(cs, &same);
+      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess && !last) e = cudaErrorUnknown;
+    }
+    if (e != cudaSuccess) {
+      cudaStreamDestroy(cs);
+      set_error("CUDA graph capture (round 1) failed: %s", cudaGetErrorString(e));
+      return HLM_B200_ERR_CUDA;
+    }
+  }
   cudaGraphNodeParams np = {};
   np.type = cudaGraphNodeTypeConditional;
   np.conditional.handle = handle;
   np.conditional.type = cudaGraphCondTypeWhile;
   np.conditional.size = 1;
   cudaGraphNode_t node;
-  CU_CHECK(cudaGraphAddNode(&node, w.graph, nullptr, 0, &np));
+  CU_CHECK(cudaGraphAddNode(&node, graph, last ? &last : nullptr, last ? 1 : 0, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
-  cudaStream_t cs;
-  CU_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   if (e == cudaSuccess) {
     const uint32_t before = L.launches;
     L.filter<true>(cs);
@@ -605,7 +650,7 @@ static int build_loop_graph(Launcher& L) {
     set_error("CUDA graph capture failed: %s", cudaGetErrorString(e));
     return HLM_B200_ERR_CUDA;
   }
-  CU_CHECK(cudaGraphInstantiate(&w.graph_exec, w.graph, 0));
+  CU_CHECK(cudaGraphInstantiate(&w.graph_exec[which], graph, 0));
   w.graph_key = L.P;
   return HLM_B200_OK;
 }
@@ -663,11 +708,29 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   P.deact_cnt = w.deact_cnt;
 
   if (!g->round_grid) {
-    int occ = 0;
-    CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_vmax_small<2, true>, kBlock, 0));
+    // persistent grids: exactly the CTAs that are resident at once; regions are handed out by ticket
+    int occ = 0, occ_sweep = 0;
+    CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_vmax_small<true>, kBlock, 0));
+    switch (g->uniform_d) {
+      case 2: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sweep, k_sweep_uniform<2, true, false>, kBlock, 0)); break;
+      case 4: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sweep, k_sweep_uniform<4, true, false>, kBlock, 0)); break;
+      case 8: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sweep, k_sweep_uniform<8, true, false>, kBlock, 0)); break;
+      default: occ_sweep = occ; break;
+    }
+    int occ_check = 0;
+    switch (g->uniform_d) {
+      case 2: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_check, k_check_commit_small<2>, kBlock, 0)); break;
+      case 4: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_check, k_check_commit_small<4>, kBlock, 0)); break;
+      case 8: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_check, k_check_commit_small<8>, kBlock, 0)); break;
+      default: CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_check, k_check_commit_small<0>, kBlock, 0)); break;
+    }
     g->round_grid = g->num_sms * std::max(1, occ);
+    g->sweep_grid = g->num_sms * std::max(1, occ_sweep);
+    g->check_grid = g->num_sms * std::max(1, occ_check);
     g->large_grid = g->num_sms * 4;
   }
+  // candidate lists are short: claim several regions per ticket, but keep every resident warp busy
+  P.check_claim = std::min<uint32_t>(kCoarseClaim, std::max<uint32_t>(1u, P.nseg / (static_cast<uint32_t>(g->check_grid) * kWarpsPerBlock)));
   return HLM_B200_OK;
 }
 
@@ -686,7 +749,10 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   RoundParams& P = L.P;
 
   bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact;
-  if (use_graph && (!w.graph_exec || !same_params(w.graph_key, P))) ST_CHECK(build_loop_graph(L));
+  if (use_graph && (!w.graph_exec[0] || !same_params(w.graph_key, P))) {
+    w.drop_graphs();
+    ST_CHECK(build_loop_graph(L, 0));
+  }
 
   CU_CHECK(cudaEventRecord(w.ev0, s));
   // per-call state
@@ -694,6 +760,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   std::memset(&c0, 0, sizeof(c0));
   c0.round = 1;
   c0.count1[0] = g->num_large;
+  c0.active_prev = g->m;
   c0.max_rounds = max_rounds;
   CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
   CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
@@ -707,7 +774,9 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
                              cudaMemcpyDeviceToDevice, s));
 
   Ctrl c = c0;
-  uint32_t tie_redo = 0, graph_launches = 0;
+  uint32_t tie_redo = 0, graph_launches = 0, graph_kernels = 0;
+  bool in_graph = false;
+  Ctrl c_before = c0;
   const bool want_times = (cfg->flags & HLM_B200_FLAG_KERNEL_TIMES) && !use_graph && !L.exact;
   std::vector<float> t_filter, t_check;
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
@@ -718,8 +787,14 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   } else {
     for (;;) {
       if (use_graph) {
-        CU_CHECK(cudaGraphLaunch(w.graph_exec, s));
+        // one launch runs every round; it only comes back early for a tie or a tag wrap, and the
+        // run is then resumed with the WHILE node alone (the full graph starts at round 1)
+        const int which = graph_launches == 0 ? 0 : 1;
+        if (!w.graph_exec[which]) ST_CHECK(build_loop_graph(L, which));
+        c_before = c;
+        CU_CHECK(cudaGraphLaunch(w.graph_exec[which], s));
         ++graph_launches;
+        in_graph = true;
       } else if (L.exact) {
         L.filter<false>(s);
         // the exact levels need the list lengths on the host
@@ -729,7 +804,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
         L.advance(s, 0, 0);
       } else {
         if (want_times) CU_CHECK(cudaEventRecord(tev[0], s));
-        L.filter<true>(s);
+        L.filter<true>(s, c.round == 1);
         if (want_times) CU_CHECK(cudaEventRecord(tev[1], s));
         L.check(s);
         if (want_times) CU_CHECK(cudaEventRecord(tev[2], s));
@@ -737,6 +812,15 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
       }
       CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
       CU_CHECK(cudaStreamSynchronize(s));
+      if (in_graph) {
+        in_graph = false;
+        // sweeps executed by this launch: rounds c_before.round .. last, where the last sweep is
+        // the one that found the lists empty / hit the cap / saw the tie (round not advanced)
+        const uint32_t last = c.status == ST_EPOCH ? c.round - 1u : c.round;
+        const uint32_t sweeps = last - c_before.round + 1u;
+        graph_kernels += graph_launches == 1 ? w.graph_head_launches + (sweeps - 1u) * w.graph_body_launches
+                                             : sweeps * w.graph_body_launches;
+      }
       if (want_times) {
         float a = 0.f, b = 0.f;
         CU_CHECK(cudaEventElapsedTime(&a, tev[0], tev[1]));
@@ -772,7 +856,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   out->graph_launches = graph_launches;
   out->device_edge_visits = c.edges_swept;
   // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
-  out->kernel_launches = L.launches + (use_graph ? (rounds + 1) * w.graph_body_launches : 0);
+  out->kernel_launches = L.launches + graph_kernels;
   for (auto& ev : tev)
     if (ev) cudaEventDestroy(ev);
   if (want_times) {

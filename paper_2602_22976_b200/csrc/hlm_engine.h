@@ -47,12 +47,16 @@ struct Workspace {
   void* pin_w = nullptr;
   uint64_t pin_cap = 0;
   // CUDA-graph WHILE loop over the round body
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;
+  // [0]: round 1 (specialised sweep) followed by the WHILE node; [1]: the WHILE node alone, used
+  // to resume after a tie redo or a tag wrap handled by the host
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
   RoundParams graph_key = {};
-  uint32_t graph_body_launches = 0;
+  uint32_t graph_head_launches = 0;  // round 1 (ahead of the WHILE node)
+  uint32_t graph_body_launches = 0;  // one iteration of the WHILE body
   uint32_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void drop_graphs();
   void release();
 };
 
@@ -85,7 +89,7 @@ struct Graph {
   uint32_t* vinc = nullptr;  // kappa
   uint64_t device_bytes = 0;
   uint64_t h2d_bytes = 0;
-  int round_grid = 0, large_grid = 0;
+  int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0;
   Workspace ws;
   CrewState* crew = nullptr;
   void* mg = nullptr;  // MgState of an edge-partitioned run in progress (hlm_multi.inc)

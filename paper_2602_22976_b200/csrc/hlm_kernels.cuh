@@ -10,24 +10,18 @@ namespace hlmb {
 // Round kernels, class 0: one thread per edge (size <= kLargeEdge), ITEMS edges per thread and
 // tile.  D > 0: uniform edge size, one 64/128-bit pin load per edge; D == 0: runtime offsets.
 // ---------------------------------------------------------------------------------------------
-#ifndef HLM_ITEMS_D2
-#define HLM_ITEMS_D2 1
-#endif
-#ifndef HLM_ITEMS_D4
-#define HLM_ITEMS_D4 1
-#endif
 #ifndef HLM_VTOP_LD
 #define HLM_VTOP_LD __ldca  // L1 may serve hub vertices: stale values are only ever too small (safe)
+#endif
+#ifndef HLM_SWEEP_MIN_BLOCKS
+#define HLM_SWEEP_MIN_BLOCKS 4  // 64 registers: four batches of a warp are in flight at once
 #endif
 #ifndef HLM_MIN_BLOCKS
 #define HLM_MIN_BLOCKS 8
 #endif
-
-template <int D>
-struct TileShape {
-  static constexpr int kItems = D == 2 ? HLM_ITEMS_D2 : (D == 4 ? HLM_ITEMS_D4 : 1);  // edges per lane and step
-  static constexpr uint32_t kStep = 32 * kItems;             // edges per warp and step
-};
+#ifndef HLM_SWEEP_PEND_D2
+#define HLM_SWEEP_PEND_D2 2  // pending-tie register sets for d = 2 (atomics looked at two steps later)
+#endif
 
 __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
                                                  uint32_t seg) {
@@ -36,14 +30,343 @@ __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool iden
   return b >= P.m ? 0u : static_cast<uint32_t>(min(static_cast<uint64_t>(P.seg_cap), P.m - b));
 }
 
-// A CTA claims kWarpsPerBlock consecutive regions by ticket; each warp then owns one region and
-// runs on its own (ballot / popc compaction, no block barrier inside the sweep).
+// One warp claims `gran` consecutive regions of the id space per ticket (no block barrier anywhere
+// in a sweep).  Same-address atomics retire at roughly one per nanosecond, so a kernel that takes
+// 75 K tickets cannot finish in less than ~60 us: sweeps over short lists claim 8 regions at a time.
+__device__ __forceinline__ uint32_t claim_region(uint32_t* ticket, uint32_t lane) {
+  uint32_t seg = 0;
+  if (lane == 0) seg = atomicAdd(ticket, 1u);
+  return __shfl_sync(0xffffffffu, seg, 0);
+}
+constexpr uint32_t kCoarseClaim = 8;
+__device__ __forceinline__ uint32_t claim_granularity(const RoundParams& P, uint32_t list_len) {
+  // keep several tickets per resident warp (dynamic balance) while the list is long
+  return list_len > (P.m >> 3) ? 1u : (list_len > (P.m >> 5) ? 2u : (list_len > (P.m >> 7) ? 4u : kCoarseClaim));
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t x) { return __reduce_add_sync(0xffffffffu, x); }
+
+// ---------------------------------------------------------------------------------------------
+// Round sweep, uniform edge size D (2, 4, 8): one thread per edge, one 64/128-bit pin load per
+// edge, software-pipelined over the 32-edge batches of a warp's region.
+//
+// A batch goes through four stages, one per step, so that every global-memory round trip of
+// batch t overlaps the work of its neighbours instead of stalling the warp (the sweep was
+// latency-bound with four dependent waits per batch: profiles/ncu_c2_r01_baseline.md):
+//   A  (batch t+3)  load the list id and the pins (streaming, evict-first); round 1 also loads
+//                   the caller id and the base weight here, because every edge survives
+//   B  (batch t+2)  gather the 32-bit filter word vtop[v] of every pin (L2-resident)
+//   C1 (batch t+1)  a pin with kTopDead kills the edge (the reference's deactivation phase,
+//                   local_max_par.hpp:229-248); survivors are compacted into the next list and
+//                   fetch caller id + base weight
+//   C2 (batch t)    key of the edge (weight refresh, :126-135), atomicMax at the pins where it can
+//                   still raise the maximum (vertex argmax, :137-159), candidate list for the
+//                   check kernel.  The returning atomics' results are only looked at (tie
+//                   detection) one or two steps later.
+// The four batches live in four statically named register sets (the loop is unrolled by four and
+// the roles rotate), so no value that is still in flight is ever moved or touched early.
+// R1: the kernel launched for round 1 (identity list in and out, no dead vertices yet).
+// ---------------------------------------------------------------------------------------------
+template <int D>
+struct SweepSlot {
+  uint32_t e;
+  bool live;
+  PinVec<D> pv;
+  uint32_t cur[D];
+  uint32_t oid;  // caller's id of the edge (before id_base)
+  double base;
+};
+
+// results of the returning atomics of one C2 step, not yet looked at
+template <int D>
+struct PendingTie {
+  unsigned long long key;
+  unsigned long long old[D];
+  __device__ __forceinline__ void clear() {
+    key = 0ull;
+#pragma unroll
+    for (int i = 0; i < D; ++i) old[i] = 1ull;
+  }
+  __device__ __forceinline__ bool hit() const {
+    bool t = false;
+#pragma unroll
+    for (int i = 0; i < D; ++i) t |= (old[i] == key);
+    return t;
+  }
+};
+
+// `old` keeps its value unless the atomic is performed: the destination register of the atomic
+// is the pending slot itself, so nothing waits for the result here.
+__device__ __forceinline__ void atomic_max_u64_if(bool pred, unsigned long long* addr, unsigned long long val,
+                                                  unsigned long long& old) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.max.u64 %0, [%1], %3;\n\t}"
+      : "+l"(old)
+      : "l"(addr), "r"(static_cast<uint32_t>(pred)), "l"(val)
+      : "memory");
+}
+
+template <int D>
+struct SweepState {
+  uint32_t out_off, cand_off, local_deact;
+  bool tie;
+};
+
+template <int D, bool VMAX, bool R1, int NPEND>
+struct SweepCtx {
+  const RoundParams& P;
+  uint32_t r, tag, lane, lt_mask;
+  bool in_ident, out_ident, peek;
+  const uint32_t* __restrict__ in;
+  uint32_t* __restrict__ out;
+  uint32_t seg_base, cnt;
+
+  // one pipeline step: stage A on `a`, B on `b`, C1 on `c1`, C2 on `c2`
+  __device__ __forceinline__ void step(uint32_t it, SweepSlot<D>& a, SweepSlot<D>& b, SweepSlot<D>& c1,
+                                       SweepSlot<D>& c2, PendingTie<D>& pend, SweepState<D>& st) const {
+    // ---- stage B: filter words of batch it-1
+#pragma unroll
+    for (int i = 0; i < D; ++i) b.cur[i] = 0u;
+    if (peek && b.live) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) b.cur[i] = HLM_VTOP_LD(P.vtop + b.pv.v[i]);
+    }
+    // ---- stage A: ids and pins of batch it
+    {
+      const uint32_t idx = it * 32u + lane;
+      a.live = idx < cnt;  // false for the drain steps
+      if (a.live) {
+        a.e = in_ident ? seg_base + idx : __ldcs(in + seg_base + idx);
+        a.pv = load_pins_stream<D>(P.csr.pins, a.e);
+        if (R1) {
+          a.oid = P.orig ? __ldcs(P.orig + a.e) : a.e;
+          a.base = base_of_stream(P, a.e);
+        }
+      }
+    }
+    // ---- stage C1: batch it-2
+    if (!R1) {
+      if (c1.live) {
+        bool dead_any = false;
+#pragma unroll
+        for (int i = 0; i < D; ++i) dead_any |= (c1.cur[i] == kTopDead);
+        if (dead_any) {
+          c1.live = false;
+          ++st.local_deact;
+        }
+      }
+      if (!out_ident) {  // order-preserving warp compaction into the next round's list
+        const uint32_t ballot = __ballot_sync(0xffffffffu, c1.live);
+        if (c1.live) __stcs(out + seg_base + st.out_off + __popc(ballot & lt_mask), c1.e);
+        st.out_off += __popc(ballot);
+      }
+      if (VMAX && c1.live) {
+        c1.oid = P.orig ? __ldg(P.orig + c1.e) : c1.e;
+        c1.base = base_of(P, c1.e);
+      }
+    }
+    // ---- stage C2: batch it-3
+    if constexpr (VMAX) {
+      bool cand = false;
+      if (c2.live) {
+        const unsigned long long key = priority_key(P.stream, P.ks, c2.oid + P.id_base, r, c2.base, tag);
+        const uint32_t hi = static_cast<uint32_t>(key >> 32);
+        bool lost = false;
+        if constexpr (NPEND > 0) {
+          st.tie |= pend.hit();  // atomics issued NPEND steps ago
+          pend.key = key;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            pend.old[i] = ~key;
+            const bool dep = c2.cur[i] <= hi;
+            atomic_max_u64_if(dep, P.vkey + c2.pv.v[i], key, pend.old[i]);
+            if (dep) atomicMax(P.vtop + c2.pv.v[i], hi);
+            lost |= !dep;  // a larger key was already there: cannot win this round
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            st.tie |= deposit_key(P, c2.pv.v[i], key, c2.cur[i]);
+            lost |= c2.cur[i] > hi;
+          }
+        }
+        cand = !lost;
+      }
+      // edges that may still win go to the (dense) candidate list of the check kernel
+      const uint32_t ballot = __ballot_sync(0xffffffffu, cand);
+      if (cand) P.cand_ids[seg_base + st.cand_off + __popc(ballot & lt_mask)] = c2.e;
+      st.cand_off += __popc(ballot);
+    }
+  }
+};
+
+template <int D>
+struct SweepTuning {  // CTAs per SM (register budget) and pending-tie sets per edge size
+  static constexpr int kMinBlocks = D == 2 ? HLM_SWEEP_MIN_BLOCKS : (D == 4 ? 3 : 2);
+  static constexpr int kPend = D == 2 ? HLM_SWEEP_PEND_D2 : (D == 4 ? 1 : 0);
+};
+
+template <int D, bool VMAX, bool R1>
+__global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_uniform(const RoundParams P) {
+  static_assert(!R1 || VMAX, "round 1 without keys has nothing to do");
+  constexpr int NPEND = SweepTuning<D>::kPend;
+  Ctrl* c = P.ctrl;
+  const uint32_t par = c->parity;
+  SweepCtx<D, VMAX, R1, NPEND> X{P};
+  X.r = c->round;
+  X.tag = round_tag(P.ks, X.r);
+  X.lane = threadIdx.x & 31;
+  X.lt_mask = (1u << X.lane) - 1u;
+  X.in_ident = R1 || X.r <= 2;   // rounds 1 and 2 read the identity list
+  X.out_ident = R1 || X.r == 1;  // round 1 keeps every edge: nothing to write
+  X.peek = X.r > 1 || P.ks.precheck;
+  X.in = P.seg_ids[par];
+  X.out = P.seg_ids[par ^ 1];
+  const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
+  uint32_t* __restrict__ out_cnt = P.seg_cnt[par ^ 1];
+  uint32_t local_kept = 0;
+  SweepState<D> st;
+  st.local_deact = 0;
+  st.tie = false;
+  PendingTie<D> pend0, pend1;
+  pend0.clear();
+  pend1.clear();
+
+  const uint32_t gran = R1 ? 1u : claim_granularity(P, c->active_prev);
+  for (uint32_t seg = 0, seg_end = 0;; ++seg) {
+    if (seg == seg_end) {
+      seg = claim_region(&c->ticket_f, X.lane) * gran;
+      seg_end = seg + gran;
+    }
+    if (seg >= P.nseg) break;
+    X.cnt = region_count(P, X.in_ident, in_cnt, seg);
+    X.seg_base = seg * P.seg_cap;
+    const uint32_t steps = ((X.cnt + 31u) >> 5) + 3u;
+    st.out_off = 0;
+    st.cand_off = 0;
+    SweepSlot<D> s0, s1, s2, s3;
+    s0.live = s1.live = s2.live = s3.live = false;
+    if (X.cnt) {
+      for (uint32_t it = 0; it < steps; it += 4u) {
+        X.step(it, s0, s3, s2, s1, pend0, st);
+        X.step(it + 1u, s1, s0, s3, s2, NPEND > 1 ? pend1 : pend0, st);
+        X.step(it + 2u, s2, s1, s0, s3, pend0, st);
+        X.step(it + 3u, s3, s2, s1, s0, NPEND > 1 ? pend1 : pend0, st);
+      }
+    }
+    if (X.lane == 0) {
+      const uint32_t kept = X.out_ident ? X.cnt : st.out_off;
+      out_cnt[seg] = kept;
+      if (VMAX) P.cand_cnt[seg] = st.cand_off;
+      local_kept += kept;
+    }
+  }
+  if constexpr (NPEND > 0) st.tie |= pend0.hit() | pend1.hit();
+  const uint32_t d = warp_sum(st.local_deact);
+  if (X.lane == 0) {
+    if (d) atomicAdd(P.deact_cnt + (X.r - 1), d);
+    if (local_kept) atomicAdd(&c->active_small, local_kept);
+  }
+  if (st.tie) c->tie_flag = 1u;
+}
+
+// Non-pipelined form of the same sweep: one batch per warp at a time, 32 registers, 64 resident
+// warps per SM.  Latency is hidden by occupancy instead of by the per-warp pipeline.
 template <int D, bool VMAX>
+__global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundParams P) {
+  Ctrl* c = P.ctrl;
+  const uint32_t r = c->round;
+  const uint32_t par = c->parity;
+  const bool in_ident = r <= 2;
+  const bool out_ident = r == 1;
+  const bool peek = r > 1 || P.ks.precheck;
+  const uint32_t* __restrict__ in = P.seg_ids[par];
+  const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
+  uint32_t* __restrict__ out = P.seg_ids[par ^ 1];
+  uint32_t* __restrict__ out_cnt = P.seg_cnt[par ^ 1];
+  const uint32_t tag = round_tag(P.ks, r);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t local_deact = 0, local_kept = 0;
+  bool tie = false;
+  const uint32_t gran = claim_granularity(P, c->active_prev);
+  for (uint32_t seg = 0, seg_end = 0;; ++seg) {
+    if (seg == seg_end) {
+      seg = claim_region(&c->ticket_f, lane) * gran;
+      seg_end = seg + gran;
+    }
+    if (seg >= P.nseg) break;
+    const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
+    const uint32_t seg_base = seg * P.seg_cap;
+    uint32_t out_off = 0, cand_off = 0;
+    for (uint32_t t0 = 0; t0 < cnt; t0 += 32u) {
+      const uint32_t idx = t0 + lane;
+      bool survive = idx < cnt, cand = false;
+      uint32_t e = 0;
+      PinVec<D> pv;
+      uint32_t cur[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) cur[i] = 0u;
+      if (survive) {
+        e = in_ident ? seg_base + idx : __ldcs(in + seg_base + idx);
+        pv = load_pins_stream<D>(P.csr.pins, e);
+        if (peek) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+          bool dead_any = false;
+#pragma unroll
+          for (int i = 0; i < D; ++i) dead_any |= (cur[i] == kTopDead);
+          if (dead_any) {
+            survive = false;
+            ++local_deact;
+          }
+        }
+      }
+      if constexpr (VMAX) {
+        if (survive) {
+          const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
+          const uint32_t hi = static_cast<uint32_t>(key >> 32);
+          bool lost = false;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            tie |= deposit_key(P, pv.v[i], key, cur[i]);
+            lost |= cur[i] > hi;
+          }
+          cand = !lost;
+        }
+      }
+      if (!out_ident) {
+        const uint32_t ballot = __ballot_sync(0xffffffffu, survive);
+        if (survive) __stcs(out + seg_base + out_off + __popc(ballot & lt_mask), e);
+        out_off += __popc(ballot);
+      }
+      if constexpr (VMAX) {
+        const uint32_t ballot = __ballot_sync(0xffffffffu, cand);
+        if (cand) P.cand_ids[seg_base + cand_off + __popc(ballot & lt_mask)] = e;
+        cand_off += __popc(ballot);
+      }
+    }
+    if (lane == 0) {
+      const uint32_t kept = out_ident ? cnt : out_off;
+      out_cnt[seg] = kept;
+      if (VMAX) P.cand_cnt[seg] = cand_off;
+      local_kept += kept;
+    }
+  }
+  const uint32_t d = warp_sum(local_deact);
+  if (lane == 0) {
+    if (d) atomicAdd(P.deact_cnt + (r - 1), d);
+    if (local_kept) atomicAdd(&c->active_small, local_kept);
+  }
+  if (tie) c->tie_flag = 1u;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Round sweep, runtime edge sizes (<= kLargeEdge pins per edge): one thread per short edge, the
+// whole warp for a medium one.
+// ---------------------------------------------------------------------------------------------
+template <bool VMAX>
 __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(const RoundParams P) {
-  constexpr int ITEMS = TileShape<D>::kItems;
-  constexpr uint32_t STEP = TileShape<D>::kStep;
-  __shared__ uint32_t s_warp[kWarpsPerBlock];
-  __shared__ uint32_t s_ticket;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -54,179 +377,114 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
   uint32_t* __restrict__ out = P.seg_ids[par ^ 1];
   uint32_t* __restrict__ out_cnt = P.seg_cnt[par ^ 1];
   const uint32_t tag = round_tag(P.ks, r);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t local_deact = 0, local_kept = 0;
   bool tie = false;
 
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&c->ticket_f, 1u);
-    __syncthreads();
-    const uint32_t seg = s_ticket * kWarpsPerBlock + warp;
-    if (s_ticket * kWarpsPerBlock >= P.nseg) break;
-    if (seg >= P.nseg) continue;
+  const uint32_t gran = claim_granularity(P, c->active_prev);
+  for (uint32_t seg = 0, seg_end = 0;; ++seg) {
+    if (seg == seg_end) {
+      seg = claim_region(&c->ticket_f, lane) * gran;
+      seg_end = seg + gran;
+    }
+    if (seg >= P.nseg) break;
     const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
     const uint32_t seg_base = seg * P.seg_cap;
     uint32_t out_off = 0, cand_off = 0;
-    for (uint32_t t0 = 0; t0 < cnt; t0 += STEP) {
-      uint32_t e[ITEMS];
-      bool survive[ITEMS], cand[ITEMS];
+    for (uint32_t t0 = 0; t0 < cnt; t0 += 32u) {
+      const uint32_t idx = t0 + lane;
+      bool survive = idx < cnt, cand = false;
+      uint32_t e = 0;
+      if (survive) e = in_ident ? seg_base + idx : in[seg_base + idx];
+      bool is_long = false;
+      uint64_t long_b = 0;
+      uint32_t long_s = 0;
+      if (survive) {
+        uint64_t b;
+        uint32_t s;
+        P.csr.range(e, b, s);
+        if (P.has_large && s > kLargeEdge) {
+          survive = false;  // class-1 edge seen through the identity list
+        } else {
+          const uint32_t* __restrict__ pp = P.csr.pins + b;
+          const bool peek = r > 1 || P.ks.precheck;
+          if (s <= 8) {
+            // short edge: every pin and its filter word in flight at once, one gather per pin
+            uint32_t v[8], cur[8];
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t idx = t0 + k * 32 + lane;
-        survive[k] = idx < cnt;
-        cand[k] = false;
-        e[k] = 0;
-        if (survive[k]) e[k] = in_ident ? seg_base + idx : in[seg_base + idx];
-      }
-      if constexpr (D > 0) {
-        PinVec<D> pv[ITEMS];
+            for (int i = 0; i < 8; ++i) v[i] = static_cast<uint32_t>(i) < s ? __ldg(pp + i) : 0u;
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
-          if (survive[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
-        // One L2 load per pin serves two purposes: kVertexDead in the slot means the vertex was
-        // covered by a matched edge (invalidation, local_max_par.hpp:229-248), anything else is
-        // the running maximum that filters the atomics below.
-        const bool peek = r > 1 || P.ks.precheck;
-        uint32_t cur[ITEMS][D];
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-#pragma unroll
-          for (int i = 0; i < D; ++i) cur[k][i] = 0u;
-        }
-        if (peek) {
-#pragma unroll
-          for (int k = 0; k < ITEMS; ++k)
-            if (survive[k]) {
-#pragma unroll
-              for (int i = 0; i < D; ++i) cur[k][i] = HLM_VTOP_LD(P.vtop + pv[k].v[i]);
-            }
-#pragma unroll
-          for (int k = 0; k < ITEMS; ++k) {
-            if (!survive[k]) continue;
+            for (int i = 0; i < 8; ++i)
+              cur[i] = (peek && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
             bool dead_any = false;
 #pragma unroll
-            for (int i = 0; i < D; ++i) dead_any |= (cur[k][i] == kTopDead);
+            for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
             if (dead_any) {
-              survive[k] = false;
+              survive = false;
               ++local_deact;
-            }
-          }
-        }
-        if constexpr (VMAX) {
-#pragma unroll
-          for (int k = 0; k < ITEMS; ++k)
-            if (survive[k]) {
+            } else if constexpr (VMAX) {
               const unsigned long long key =
-                  priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
+                  priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
               const uint32_t hi = static_cast<uint32_t>(key >> 32);
               bool lost = false;
 #pragma unroll
-              for (int i = 0; i < D; ++i) {
-                tie |= deposit_key(P, pv[k].v[i], key, cur[k][i]);
-                lost |= cur[k][i] > hi;  // a larger key was already there: cannot win this round
-              }
-              cand[k] = !lost;
-            }
-        }
-      } else {
-        // runtime sizes: ITEMS == 1
-        bool is_long = false;
-        uint64_t long_b = 0;
-        uint32_t long_s = 0;
-        if (survive[0]) {
-          uint64_t b;
-          uint32_t s;
-          P.csr.range(e[0], b, s);
-          if (P.has_large && s > kLargeEdge) {
-            survive[0] = false;  // class-1 edge seen through the identity list
-          } else {
-            const uint32_t* __restrict__ pp = P.csr.pins + b;
-            const bool peek = r > 1 || P.ks.precheck;
-            if (s <= 8) {
-              // short edge: every pin and its filter word in flight at once, one gather per pin
-              uint32_t v[8], cur[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = static_cast<uint32_t>(i) < s ? __ldg(pp + i) : 0u;
-#pragma unroll
               for (int i = 0; i < 8; ++i)
-                cur[i] = (peek && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
-              bool dead_any = false;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
-              if (dead_any) {
-                survive[0] = false;
-                ++local_deact;
-              } else if constexpr (VMAX) {
-                const unsigned long long key =
-                    priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
-                const uint32_t hi = static_cast<uint32_t>(key >> 32);
-                bool lost = false;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  if (static_cast<uint32_t>(i) < s) {
-                    tie |= deposit_key(P, v[i], key, cur[i]);
-                    lost |= cur[i] > hi;
-                  }
-                cand[0] = !lost;
-              }
-            } else {
-              is_long = true;  // 9..32 pins: handled below by the whole warp, one pin per lane
-              long_b = b;
-              long_s = s;
+                if (static_cast<uint32_t>(i) < s) {
+                  tie |= deposit_key(P, v[i], key, cur[i]);
+                  lost |= cur[i] > hi;
+                }
+              cand = !lost;
             }
+          } else {
+            is_long = true;  // 9..32 pins: handled below by the whole warp, one pin per lane
+            long_b = b;
+            long_s = s;
           }
         }
-        // medium edges, one at a time, cooperatively: the 32 lanes take one pin each, so an edge
-        // costs one gather round trip instead of one per pin
-        uint32_t long_mask = __ballot_sync(0xffffffffu, is_long);
-        while (long_mask) {
-          const int src = __ffs(long_mask) - 1;
-          long_mask &= long_mask - 1;
-          const uint64_t eb = __shfl_sync(0xffffffffu, long_b, src);
-          const uint32_t es = __shfl_sync(0xffffffffu, long_s, src);
-          const uint32_t ee = __shfl_sync(0xffffffffu, e[0], src);
-          const bool mine = lane < es;
-          const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
-          const bool peek = r > 1 || P.ks.precheck;
-          const uint32_t cur = (mine && peek) ? HLM_VTOP_LD(P.vtop + v) : 0u;
-          const bool dead_any = __any_sync(0xffffffffu, mine && cur == kTopDead);
-          bool lost = false;
-          if (!dead_any) {
-            if constexpr (VMAX) {
-              const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, ee), r, base_of(P, ee), tag);
-              if (mine) tie |= deposit_key(P, v, key, cur);
-              lost = __any_sync(0xffffffffu, mine && cur > static_cast<uint32_t>(key >> 32));
-            }
+      }
+      // medium edges, one at a time, cooperatively: the 32 lanes take one pin each, so an edge
+      // costs one gather round trip instead of one per pin
+      uint32_t long_mask = __ballot_sync(0xffffffffu, is_long);
+      while (long_mask) {
+        const int src = __ffs(long_mask) - 1;
+        long_mask &= long_mask - 1;
+        const uint64_t eb = __shfl_sync(0xffffffffu, long_b, src);
+        const uint32_t es = __shfl_sync(0xffffffffu, long_s, src);
+        const uint32_t ee = __shfl_sync(0xffffffffu, e, src);
+        const bool mine = lane < es;
+        const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
+        const bool peek = r > 1 || P.ks.precheck;
+        const uint32_t cur = (mine && peek) ? HLM_VTOP_LD(P.vtop + v) : 0u;
+        const bool dead_any = __any_sync(0xffffffffu, mine && cur == kTopDead);
+        bool lost = false;
+        if (!dead_any) {
+          if constexpr (VMAX) {
+            const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, ee), r, base_of(P, ee), tag);
+            if (mine) tie |= deposit_key(P, v, key, cur);
+            lost = __any_sync(0xffffffffu, mine && cur > static_cast<uint32_t>(key >> 32));
           }
-          if (static_cast<int>(lane) == src) {
-            if (dead_any) {
-              survive[0] = false;
-              ++local_deact;
-            } else if (VMAX) {
-              cand[0] = !lost;
-            }
+        }
+        if (static_cast<int>(lane) == src) {
+          if (dead_any) {
+            survive = false;
+            ++local_deact;
+          } else if (VMAX) {
+            cand = !lost;
           }
         }
       }
       if (!out_ident) {
         // order-preserving warp compaction
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const uint32_t ballot = __ballot_sync(0xffffffffu, survive[k]);
-          if (survive[k]) out[seg_base + out_off + __popc(ballot & lt_mask)] = e[k];
-          out_off += __popc(ballot);
-        }
+        const uint32_t ballot = __ballot_sync(0xffffffffu, survive);
+        if (survive) out[seg_base + out_off + __popc(ballot & lt_mask)] = e;
+        out_off += __popc(ballot);
       }
       if constexpr (VMAX) {
         // edges that may still win go to the (dense) candidate list of the check kernel
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const uint32_t ballot = __ballot_sync(0xffffffffu, cand[k]);
-          if (cand[k]) P.cand_ids[seg_base + cand_off + __popc(ballot & lt_mask)] = e[k];
-          cand_off += __popc(ballot);
-        }
+        const uint32_t ballot = __ballot_sync(0xffffffffu, cand);
+        if (cand) P.cand_ids[seg_base + cand_off + __popc(ballot & lt_mask)] = e;
+        cand_off += __popc(ballot);
       }
     }
     if (lane == 0) {
@@ -236,66 +494,84 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
       local_kept += kept;
     }
   }
-  const uint32_t d = block_sum(local_deact, s_warp);
-  if (threadIdx.x == 0 && d) atomicAdd(P.deact_cnt + (r - 1), d);
-  const uint32_t kept = block_sum(local_kept, s_warp);
-  if (threadIdx.x == 0 && kept) atomicAdd(&c->active_small, kept);
+  const uint32_t d = warp_sum(local_deact);
+  if (lane == 0) {
+    if (d) atomicAdd(P.deact_cnt + (r - 1), d);
+    if (local_kept) atomicAdd(&c->active_small, local_kept);
+  }
   if (tie) c->tie_flag = 1u;
 }
 
+// Check + commit over the candidate lists (local_max_par.hpp:202-224): a candidate is matched iff
+// its key is the maximum at every pin; matched edges record their round and kill their pins.
+// A warp claims P.check_claim (<= kCoarseClaim) consecutive regions and walks the concatenation of their (short)
+// candidate lists, kCheckItems candidates per lane and step, so that several independent chains
+// list id -> pins -> filter word are in flight per thread.
+constexpr int kCheckItems = 4;
+
 template <int D>
-__global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_check_commit_small(const RoundParams P) {
-  constexpr int ITEMS = TileShape<D>::kItems;
-  constexpr uint32_t STEP = TileShape<D>::kStep;
-  __shared__ uint32_t s_warp[kWarpsPerBlock];
-  __shared__ uint32_t s_ticket;
+__global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundParams P) {
+  constexpr int ITEMS = D > 0 ? kCheckItems : 1;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
-  const uint32_t par = c->parity;
   const uint32_t* __restrict__ list = P.cand_ids;
   const uint32_t* __restrict__ list_cnt = P.cand_cnt;
   const uint32_t tag = round_tag(P.ks, r);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   uint32_t local_matched = 0;
 
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&c->ticket_c, 1u);
-    __syncthreads();
-    const uint32_t seg = s_ticket * kWarpsPerBlock + warp;
-    if (s_ticket * kWarpsPerBlock >= P.nseg) break;
-    if (seg >= P.nseg) continue;
-    const uint32_t cnt = list_cnt[seg];
-    const uint32_t seg_base = seg * P.seg_cap;
-    for (uint32_t t0 = 0; t0 < cnt; t0 += STEP) {
+    const uint32_t seg0 = claim_region(&c->ticket_c, lane) * P.check_claim;
+    if (seg0 >= P.nseg) break;
+    // end[j] = candidates in regions seg0 .. seg0+j (inclusive prefix), the same in every lane
+    uint32_t mine = (lane < P.check_claim && seg0 + lane < P.nseg) ? list_cnt[seg0 + lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < static_cast<int>(kCoarseClaim); o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, mine, o);
+      if (lane >= static_cast<uint32_t>(o)) mine += t;
+    }
+    uint32_t end[kCoarseClaim];
+#pragma unroll
+    for (int j = 0; j < static_cast<int>(kCoarseClaim); ++j) end[j] = __shfl_sync(0xffffffffu, mine, j);
+    const uint32_t total = end[kCoarseClaim - 1];
+    for (uint32_t t0 = 0; t0 < total; t0 += 32u * ITEMS) {
       uint32_t e[ITEMS];
-      bool valid[ITEMS], win[ITEMS];
+      bool valid[ITEMS];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t idx = t0 + k * 32 + lane;
-        valid[k] = idx < cnt;
-        win[k] = false;
-        e[k] = valid[k] ? list[seg_base + idx] : 0u;
+        const uint32_t idx = t0 + k * 32u + lane;
+        valid[k] = idx < total;
+        uint32_t j = 0, begin = 0;
+#pragma unroll
+        for (int q = 0; q + 1 < static_cast<int>(kCoarseClaim); ++q)
+          if (idx >= end[q]) {
+            j = q + 1;
+            begin = end[q];
+          }
+        e[k] = valid[k] ? list[static_cast<size_t>(seg0 + j) * P.seg_cap + (idx - begin)] : 0u;
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
+        uint32_t top0[ITEMS];
         unsigned long long key[ITEMS];
-        uint32_t top[ITEMS];
+        bool win[ITEMS];
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (valid[k]) pv[k] = load_pins<D>(P.csr.pins, e[k]);
-        // 32-bit filter word of the first pin of every item in flight together; most edges lose
-        // right here (and with the edges sorted by first pin these loads are coalesced)
+        // 32-bit filter word of the first pin first: most candidates lose right here, and with
+        // the edges sorted by first pin this load is nearly coalesced
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-          if (valid[k]) top[k] = __ldcg(P.vtop + pv[k].v[0]);
+          if (valid[k]) top0[k] = __ldcg(P.vtop + pv[k].v[0]);
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
+        for (int k = 0; k < ITEMS; ++k) {
+          win[k] = false;
           if (valid[k]) {
             key[k] = priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
-            win[k] = top[k] == static_cast<uint32_t>(key[k] >> 32);
+            win[k] = top0[k] == static_cast<uint32_t>(key[k] >> 32);
           }
+        }
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           if (win[k]) {
@@ -314,14 +590,12 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_check_commit_small(c
             for (int i = 0; i < D; ++i) full[i] = __ldcg(P.vkey + pv[k].v[i]);
 #pragma unroll
             for (int i = 0; i < D; ++i) win[k] &= (full[i] == key[k]);
-          }
+            if (win[k]) {
+              mark_matched(P, e[k], r);
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
-          if (win[k]) {
-            mark_matched(P, e[k], r);
-#pragma unroll
-            for (int i = 0; i < D; ++i) mark_dead(P, pv[k].v[i]);
-            ++local_matched;
+              for (int i = 0; i < D; ++i) mark_dead(P, pv[k].v[i]);
+              ++local_matched;
+            }
           }
       } else {
         if (valid[0]) {
@@ -342,14 +616,13 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_check_commit_small(c
               }
               ++local_matched;
             }
-            win[0] = w;
           }
         }
       }
     }
   }
-  const uint32_t t = block_sum(local_matched, s_warp);
-  if (threadIdx.x == 0 && t) atomicAdd(P.matched_cnt + r, t);
+  const uint32_t t = warp_sum(local_matched);
+  if (lane == 0 && t) atomicAdd(P.matched_cnt + r, t);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -456,6 +729,7 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
     c->rounds_done = r - 1;
   } else {
     c->edges_swept += active;
+    c->active_prev = c->active_small;
     c->active_small = 0;
     c->parity = par ^ 1;
     c->count1[par] = 0;

@@ -51,7 +51,7 @@ struct Ctrl {
   uint32_t status;
   uint32_t max_rounds;
   uint32_t rounds_done;
-  uint32_t pad;
+  uint32_t active_prev;  // class-0 edges in the list the next sweep reads (0 before round 2)
   unsigned long long edges_swept;  // sum over rounds of the active-list lengths
 };
 
@@ -99,6 +99,7 @@ struct RoundParams {
   uint32_t* seg_cnt[2];      // [buffer][nseg] ids in use per region
   uint32_t nseg;
   uint32_t seg_cap;
+  uint32_t check_claim;      // regions a warp of the check kernel claims per ticket (1..8)
   uint32_t* cand_ids;        // class 0, same regions: edges that did not lose during vertex-max
   uint32_t* cand_cnt;        // [nseg]
   // class 1: appended list
@@ -187,6 +188,33 @@ __device__ __forceinline__ PinVec<8> load_pins<8>(const uint32_t* pins, uint32_t
   const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(pins) + 2ull * e);
   const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(pins) + 2ull * e + 1);
   return {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w}};
+}
+
+// Streaming (evict-first) variants for data a sweep reads exactly once: the pin rows, the id
+// lists, the caller ids and the base weights must not push the per-vertex arrays out of L2.
+template <int D>
+__device__ __forceinline__ PinVec<D> load_pins_stream(const uint32_t* pins, uint32_t e);
+template <>
+__device__ __forceinline__ PinVec<2> load_pins_stream<2>(const uint32_t* pins, uint32_t e) {
+  const uint2 q = __ldcs(reinterpret_cast<const uint2*>(pins) + e);
+  return {{q.x, q.y}};
+}
+template <>
+__device__ __forceinline__ PinVec<4> load_pins_stream<4>(const uint32_t* pins, uint32_t e) {
+  const uint4 q = __ldcs(reinterpret_cast<const uint4*>(pins) + e);
+  return {{q.x, q.y, q.z, q.w}};
+}
+template <>
+__device__ __forceinline__ PinVec<8> load_pins_stream<8>(const uint32_t* pins, uint32_t e) {
+  const uint4 q0 = __ldcs(reinterpret_cast<const uint4*>(pins) + 2ull * e);
+  const uint4 q1 = __ldcs(reinterpret_cast<const uint4*>(pins) + 2ull * e + 1);
+  return {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w}};
+}
+__device__ __forceinline__ uint32_t edge_gid_stream(const RoundParams& P, uint32_t e) {
+  return (P.orig ? __ldcs(P.orig + e) : e) + P.id_base;
+}
+__device__ __forceinline__ double base_of_stream(const RoundParams& P, uint32_t e) {
+  return P.base ? __ldcs(P.base + e) : P.base_const;
 }
 
 // Block-wide exclusive offset of `flag` plus the block total (warp ballot + scan of 8 warp sums).
