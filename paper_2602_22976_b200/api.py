@@ -174,25 +174,44 @@ def _take(ptr, count, dtype):
     return np.ctypeslib.as_array(ptr, shape=(int(count),)).astype(dtype, copy=True)
 
 
+class _ResultOwner:
+    """Keeps an hlm_b200_result alive while numpy views of its arrays exist (no copy of the
+    matched ids: they stay in the library's page-locked result buffers until garbage-collected)."""
+
+    def __init__(self, res: _lib.Result):
+        self.res = res
+
+    def __del__(self):
+        try:
+            _lib.load_library().hlm_b200_result_free(C.byref(self.res))
+        except Exception:
+            pass
+
+
+def _borrow(owner: _ResultOwner, ptr, count, ctype, dtype):
+    if count == 0 or not ptr:
+        return np.zeros(0, dtype=dtype)
+    buf = (ctype * int(count)).from_address(C.addressof(ptr.contents))
+    buf._owner = owner  # the view keeps the buffer object, the buffer object keeps the result
+    return np.frombuffer(buf, dtype=dtype)
+
+
 def _convert(status: int, res: _lib.Result) -> MatchResult:
-    lib = _lib.load_library()
-    try:
-        if status not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
-            _raise(status, "hlm_b200_match")
-        matched = _take(res.matched_edges, res.num_matched, np.uint32)
-        round_of = _take(res.matched_round, res.num_matched, np.uint16) if res.matched_round else None
-        prm = _take(res.per_round_matched, res.rounds, np.uint32).tolist()
-        prd = _take(res.per_round_deactivated, res.rounds, np.uint32).tolist()
-        matching = Matching(matched, float(res.total_weight), int(res.rounds), prm)
-        report = RunReport(int(res.rounds), prm, prd, round_of,
-                           WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits)),
-                           float(res.wall_time_ms), int(res.write_conflicts), float(res.device_ms),
-                           int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
-                           int(res.graph_launches), matched,
-                           _take(res.round_filter_ms, res.rounds + 1, np.float32).tolist() if res.round_filter_ms else None,
-                           _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None)
-    finally:
-        lib.hlm_b200_result_free(C.byref(res))
+    owner = _ResultOwner(res)
+    if status not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
+        _raise(status, "hlm_b200_match")
+    matched = _borrow(owner, res.matched_edges, res.num_matched, C.c_uint32, np.uint32)
+    round_of = _borrow(owner, res.matched_round, res.num_matched, C.c_uint16, np.uint16) if res.matched_round else None
+    prm = _take(res.per_round_matched, res.rounds, np.uint32).tolist()
+    prd = _take(res.per_round_deactivated, res.rounds, np.uint32).tolist()
+    matching = Matching(matched, float(res.total_weight), int(res.rounds), prm)
+    report = RunReport(int(res.rounds), prm, prd, round_of,
+                       WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits)),
+                       float(res.wall_time_ms), int(res.write_conflicts), float(res.device_ms),
+                       int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
+                       int(res.graph_launches), matched,
+                       _take(res.round_filter_ms, res.rounds + 1, np.float32).tolist() if res.round_filter_ms else None,
+                       _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None)
     if status == _lib.ERR_ROUND_LIMIT:
         raise RoundLimitError(matching, report)
     return MatchResult(matching, report)

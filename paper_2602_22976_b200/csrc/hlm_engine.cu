@@ -9,8 +9,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/hlm_b200.h"
@@ -117,6 +119,72 @@ void pool_free(void* p) {
 
 static void dev_free(void* p) { pool_free(p); }
 
+// ---------------------------------------------------------------------------------------------
+// Result arrays handed to the caller (matched ids, rounds) live in page-locked host memory taken
+// from a small process-wide pool: the device-to-host copy lands directly in the caller's array
+// (no staging copy, no page faults on a fresh malloc), and hlm_b200_result_free returns the block
+// to the pool.  Falls back to malloc when pinning fails.
+// ---------------------------------------------------------------------------------------------
+namespace {
+struct HostBlock {
+  void* p;
+  size_t cap;
+};
+std::mutex g_host_mu;
+std::vector<HostBlock> g_host_free;
+std::unordered_map<void*, size_t> g_host_live;  // pinned blocks currently owned by a result
+constexpr size_t kHostPoolKeep = 16;             // free blocks kept for reuse
+}  // namespace
+
+void* host_result_alloc(size_t bytes) {
+  if (bytes == 0) bytes = 1;
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    size_t best = g_host_free.size();
+    for (size_t i = 0; i < g_host_free.size(); ++i)
+      if (g_host_free[i].cap >= bytes && (best == g_host_free.size() || g_host_free[i].cap < g_host_free[best].cap))
+        best = i;
+    if (best != g_host_free.size() && g_host_free[best].cap <= 4 * bytes + (1u << 20)) {
+      HostBlock b = g_host_free[best];
+      g_host_free.erase(g_host_free.begin() + best);
+      g_host_live[b.p] = b.cap;
+      return b.p;
+    }
+  }
+  const size_t cap = bytes + bytes / 4 + 4096;
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_live[p] = cap;
+    return p;
+  }
+  cudaGetLastError();
+  return std::malloc(bytes);
+}
+
+void host_result_free(void* p) {
+  if (!p) return;
+  HostBlock drop = {nullptr, 0};
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_live.find(p);
+    if (it == g_host_live.end()) {
+      std::free(p);
+      return;
+    }
+    g_host_free.push_back({p, it->second});
+    g_host_live.erase(it);
+    if (g_host_free.size() > kHostPoolKeep) {  // drop the smallest
+      size_t k = 0;
+      for (size_t i = 1; i < g_host_free.size(); ++i)
+        if (g_host_free[i].cap < g_host_free[k].cap) k = i;
+      drop = g_host_free[k];
+      g_host_free.erase(g_host_free.begin() + k);
+    }
+  }
+  if (drop.p) cudaFreeHost(drop.p);
+}
+
 void Workspace::release() {
   dev_free(ctrl);
   dev_free(vkey);
@@ -142,8 +210,6 @@ void Workspace::release() {
   dev_free(out_round);
   dev_free(out_w);
   dev_free(int_sum);
-  if (pin_ids) cudaFreeHost(pin_ids);
-  if (pin_round) cudaFreeHost(pin_round);
   if (pin_w) cudaFreeHost(pin_w);
   drop_graphs();
   if (ev0) cudaEventDestroy(ev0);
@@ -873,15 +939,11 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
 }
 
 static int ensure_pinned(Workspace& w, uint64_t total, bool need_w) {
-  if (total <= w.pin_cap && (!need_w || w.pin_w)) return HLM_B200_OK;
-  if (w.pin_ids) cudaFreeHost(w.pin_ids);
-  if (w.pin_round) cudaFreeHost(w.pin_round);
+  if (!need_w || (total <= w.pin_cap && w.pin_w)) return HLM_B200_OK;
   if (w.pin_w) cudaFreeHost(w.pin_w);
-  w.pin_ids = w.pin_round = w.pin_w = nullptr;
+  w.pin_w = nullptr;
   w.pin_cap = total + total / 8 + 1024;
-  CU_CHECK(cudaHostAlloc(&w.pin_ids, w.pin_cap * 4, cudaHostAllocDefault));
-  CU_CHECK(cudaHostAlloc(&w.pin_round, w.pin_cap * 2, cudaHostAllocDefault));
-  if (need_w) CU_CHECK(cudaHostAlloc(&w.pin_w, w.pin_cap * 8, cudaHostAllocDefault));
+  CU_CHECK(cudaHostAlloc(&w.pin_w, w.pin_cap * 8, cudaHostAllocDefault));
   return HLM_B200_OK;
 }
 
@@ -921,8 +983,8 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   ST_CHECK(ensure_pinned(w, total, need_w));
   out->num_matched = total;
   out->rounds = rounds;
-  out->matched_edges = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (total + 1)));
-  out->matched_round = want_round ? static_cast<uint16_t*>(std::malloc(sizeof(uint16_t) * (total + 1))) : nullptr;
+  out->matched_edges = static_cast<uint32_t*>(host_result_alloc(sizeof(uint32_t) * (total + 1)));
+  out->matched_round = want_round ? static_cast<uint16_t*>(host_result_alloc(sizeof(uint16_t) * (total + 1))) : nullptr;
   out->per_round_matched = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
   out->per_round_deactivated = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
   if (!out->matched_edges || !out->per_round_matched || !out->per_round_deactivated ||
@@ -937,8 +999,9 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
         w.mbits, w.mbits_words, w.chunk_cnt, w.mround, g->base, g->id_base, w.out_ids,
         want_round ? w.out_round : nullptr, need_w ? w.out_w : nullptr, int_sum ? w.int_sum : nullptr);
     out->kernel_launches += 1;
-    CU_CHECK(cudaMemcpyAsync(w.pin_ids, w.out_ids, total * 4, cudaMemcpyDeviceToHost, s));
-    if (want_round) CU_CHECK(cudaMemcpyAsync(w.pin_round, w.out_round, total * 2, cudaMemcpyDeviceToHost, s));
+    // straight into the caller's (page-locked) arrays
+    CU_CHECK(cudaMemcpyAsync(out->matched_edges, w.out_ids, total * 4, cudaMemcpyDeviceToHost, s));
+    if (want_round) CU_CHECK(cudaMemcpyAsync(out->matched_round, w.out_round, total * 2, cudaMemcpyDeviceToHost, s));
     if (need_w) CU_CHECK(cudaMemcpyAsync(w.pin_w, w.out_w, total * 8, cudaMemcpyDeviceToHost, s));
     if (int_sum) CU_CHECK(cudaMemcpyAsync(&isum, w.int_sum, 8, cudaMemcpyDeviceToHost, s));
   }
@@ -954,10 +1017,6 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   float ms = 0.f;
   CU_CHECK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   out->device_ms = ms;
-  if (total) {
-    std::memcpy(out->matched_edges, w.pin_ids, total * 4);
-    if (want_round) std::memcpy(out->matched_round, w.pin_round, total * 2);
-  }
   // total_weight accumulates base weights in ascending-id order (local_max_seq.hpp:79)
   // (weight_before: the ordered sum over the lower-id shards of an edge-partitioned run)
   double tw = weight_before;
@@ -1229,8 +1288,8 @@ int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result*
 
 void hlm_b200_result_free(hlm_b200_result* r) {
   if (!r) return;
-  std::free(r->matched_edges);
-  std::free(r->matched_round);
+  host_result_free(r->matched_edges);
+  host_result_free(r->matched_round);
   std::free(r->per_round_matched);
   std::free(r->per_round_deactivated);
   std::free(r->round_filter_ms);

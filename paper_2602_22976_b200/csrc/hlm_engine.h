@@ -41,9 +41,7 @@ struct Workspace {
   double* out_w = nullptr;
   uint64_t out_cap = 0;
   unsigned long long* int_sum = nullptr;
-  // pinned host staging for the device-to-host copy of the result
-  void* pin_ids = nullptr;
-  void* pin_round = nullptr;
+  // pinned host staging of the matched base weights (ordered FP64 sum on the host)
   void* pin_w = nullptr;
   uint64_t pin_cap = 0;
   // CUDA-graph WHILE loop over the round body
@@ -104,6 +102,8 @@ cudaError_t pool_malloc(void** p, size_t bytes);
 void pool_free(void* p);
 
 void set_error(const char* fmt, ...);
+void* host_result_alloc(size_t bytes);
+void host_result_free(void* p);
 uint32_t default_max_rounds(uint32_t m);
 int new_graph(int device, Graph** out);
 int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins);
