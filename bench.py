@@ -334,9 +334,11 @@ def main():
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     d2h = int(eres.matching.matched_edges.nbytes + eres.report.matched_round.nbytes + 8 * eres.report.rounds)
     assert np.array_equal(eres.matching.matched_edges, res.matching.matched_edges)
-    e2e = {"value": kappa / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
-           "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-           "call": "hlm_b200_match_host (upload + loader kernels + matching + result copy), pinned host CSR"}
+    e2e = {"value": kappa / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(eres.report.h2d_bytes),
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+           "host_input_bytes": int(h2d),
+           "call": "hlm_b200_match_host (host scan/pack of offsets+weights || pin upload, loader kernels, matching, "
+                   "result copy), pinned host CSR"}
     del host
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,

@@ -108,6 +108,7 @@ typedef struct {
    * list); NULL otherwise.  filter = k_filter_vmax (all classes), check = k_check_commit. */
   float* round_filter_ms;
   float* round_check_ms;
+  uint64_t h2d_bytes;              /* hlm_b200_match_host: bytes the loader moved host -> device */
 } hlm_b200_result;
 
 typedef struct hlm_b200_graph hlm_b200_graph; /* opaque: instance resident in HBM */

@@ -37,7 +37,8 @@ class Result(C.Structure):
                 ("wall_time_ms", C.c_double), ("device_ms", C.c_double),
                 ("tie_redo_rounds", C.c_uint32), ("kernel_launches", C.c_uint32),
                 ("graph_launches", C.c_uint32), ("write_conflicts", C.c_uint32),
-                ("round_filter_ms", C.POINTER(C.c_float)), ("round_check_ms", C.POINTER(C.c_float))]
+                ("round_filter_ms", C.POINTER(C.c_float)), ("round_check_ms", C.POINTER(C.c_float)),
+                ("h2d_bytes", C.c_uint64)]
 
 
 class GraphInfo(C.Structure):

@@ -132,6 +132,7 @@ class RunReport:
     _matched_edges: Optional[np.ndarray] = None
     round_filter_ms: Optional[List[float]] = None
     round_check_ms: Optional[List[float]] = None
+    h2d_bytes: int = 0  # run_variant (host arrays in): bytes the loader moved host -> device
 
     @property
     def matched_per_round(self) -> List[np.ndarray]:
@@ -211,7 +212,8 @@ def _convert(status: int, res: _lib.Result) -> MatchResult:
                        int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
                        int(res.graph_launches), matched,
                        _take(res.round_filter_ms, res.rounds + 1, np.float32).tolist() if res.round_filter_ms else None,
-                       _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None)
+                       _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None,
+                       int(res.h2d_bytes))
     if status == _lib.ERR_ROUND_LIMIT:
         raise RoundLimitError(matching, report)
     return MatchResult(matching, report)

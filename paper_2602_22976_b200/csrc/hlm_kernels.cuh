@@ -876,6 +876,12 @@ __global__ void k_narrow_offsets(const uint64_t* off64, uint32_t* off32, uint64_
     off32[i] = static_cast<uint32_t>(off64[i]);
 }
 
+// loader: weights the host packed to one byte each (integers 1..255) back to the resident f64 form
+__global__ void k_expand_u8(const uint8_t* __restrict__ codes, uint32_t m, double* __restrict__ base) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    base[e] = static_cast<double>(codes[e]);
+}
+
 __global__ void k_collect_large(const EdgeCsr csr, uint32_t m, uint32_t* list, uint32_t* count) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     uint64_t b;
