@@ -197,8 +197,8 @@ void Workspace::release() {
   for (int b = 0; b < 2; ++b) {
     dev_free(seg_ids[b]);
     dev_free(seg_cnt[b]);
-    dev_free(list1[b]);
   }
+  dev_free(large_state);
   dev_free(cand_ids);
   dev_free(cand_cnt);
   dev_free(matched_cnt);
@@ -595,8 +595,8 @@ int ensure_workspace(Graph* g, uint32_t max_rounds) {
     for (int b = 0; b < 2; ++b) {
       ST_CHECK(dev_alloc(&w.seg_ids[b], static_cast<size_t>(w.nseg) * w.seg_cap, g));
       ST_CHECK(dev_alloc(&w.seg_cnt[b], w.nseg, g));
-      ST_CHECK(dev_alloc(&w.list1[b], g->num_large, g));
     }
+    ST_CHECK(dev_alloc(&w.large_state, g->num_large, g));
     ST_CHECK(dev_alloc(&w.cand_ids, static_cast<size_t>(w.nseg) * w.seg_cap, g));
     ST_CHECK(dev_alloc(&w.cand_cnt, w.nseg, g));
     w.num_chunks = (w.mbits_words + kAsmChunkWords - 1) / kAsmChunkWords;
@@ -770,9 +770,8 @@ static int exact_round(Launcher& L, uint32_t r, uint32_t buf, const Ctrl& c) {
     X[cls].cls = cls;
     X[cls].buf = buf;
     X[cls].ident = r == 1;
-    X[cls].count1 = c.count1[buf];
   }
-  const uint64_t slots[2] = {static_cast<uint64_t>(w.nseg) * w.seg_cap, c.count1[buf]};
+  const uint64_t slots[2] = {static_cast<uint64_t>(w.nseg) * w.seg_cap, g->num_large};
   for (int lv = 1; lv <= 4; ++lv) {
     for (int cls = 0; cls < 2; ++cls) {
       if (slots[cls] == 0) continue;
@@ -899,8 +898,10 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   for (int b = 0; b < 2; ++b) {
     P.seg_ids[b] = w.seg_ids[b];
     P.seg_cnt[b] = w.seg_cnt[b];
-    P.list1[b] = w.list1[b];
   }
+  P.large_ids = g->large_list;
+  P.large_state = w.large_state;
+  P.num_large = g->num_large;
   P.nseg = w.nseg;
   P.seg_cap = w.seg_cap;
   P.cand_ids = w.cand_ids;
@@ -930,6 +931,11 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
     g->check_grid = g->num_sms * std::max(1, occ_check);
     g->large_grid = g->num_sms * 4;
   }
+  // large-edge list: enough chunks for ~8 per warp of the grid, at most 32 entries per chunk
+  P.large_chunk = 1;
+  while (P.large_chunk < 32u &&
+         static_cast<uint64_t>(P.num_large) / (P.large_chunk * 2u) >= static_cast<uint64_t>(g->large_grid) * kWarpsPerBlock * 8u)
+    P.large_chunk *= 2u;
   // candidate lists are short: claim several regions per ticket, but keep every resident warp busy
   P.check_claim = std::min<uint32_t>(kCoarseClaim, std::max<uint32_t>(1u, P.nseg / (static_cast<uint32_t>(g->check_grid) * kWarpsPerBlock)));
   return HLM_B200_OK;
@@ -970,9 +976,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
   CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
-  if (g->num_large)
-    CU_CHECK(cudaMemcpyAsync(w.list1[0], g->large_list, static_cast<size_t>(g->num_large) * 4,
-                             cudaMemcpyDeviceToDevice, s));
+  if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
 
   Ctrl c = c0;
   uint32_t tie_redo = 0, graph_launches = 0, graph_kernels = 0;

@@ -22,7 +22,7 @@ struct Workspace {
   uint32_t* seg_ids[2] = {nullptr, nullptr};
   uint32_t* seg_cnt[2] = {nullptr, nullptr};
   uint32_t nseg = 0, seg_cap = 0;
-  uint32_t* list1[2] = {nullptr, nullptr};
+  uint8_t* large_state = nullptr;
   uint32_t* cand_ids = nullptr;
   uint32_t* cand_cnt = nullptr;
   uint32_t* matched_cnt = nullptr;

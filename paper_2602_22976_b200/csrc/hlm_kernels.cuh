@@ -628,44 +628,69 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
 // ---------------------------------------------------------------------------------------------
 // Round kernels, class 1: one warp per large edge (ballot / shuffle reductions over its pins).
 // ---------------------------------------------------------------------------------------------
+// The large edges are few (a few percent at most), so their list is never compacted: a state
+// byte per entry says whether the edge is still active and whether it can still win this round
+// (an appended list costs one same-address atomic per surviving edge: 2.4 M of them took 7 ms on
+// the power-law instance).
+enum LargeState : uint8_t { LARGE_DROPPED = 0, LARGE_ACTIVE = 1, LARGE_CANDIDATE = 2 };
+
 template <bool VMAX>
 __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
-  const uint32_t cnt = c->count1[par];
-  const uint32_t* __restrict__ in = P.list1[par];
-  uint32_t* __restrict__ out = P.list1[par ^ 1];
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
-  uint32_t local_deact = 0;
+  uint32_t local_deact = 0, local_alive = 0;
   bool tie = false;
-  for (uint32_t pos = warp; pos < cnt; pos += nwarps) {
-    const uint32_t e = in[pos];
+  // a warp takes 32 consecutive entries: one coalesced load of their state bytes, then the active
+  // ones in turn, each with all 32 lanes
+  const uint32_t ch = P.large_chunk;  // 1..32 entries per warp and step (fewer when the list is short)
+  for (uint32_t chunk = warp; static_cast<uint64_t>(chunk) * ch < P.num_large; chunk += nwarps) {
+   const uint32_t my_pos = chunk * ch + lane;
+   uint32_t todo = __ballot_sync(0xffffffffu,
+                                 lane < ch && my_pos < P.num_large && P.large_state[my_pos] != LARGE_DROPPED);
+   while (todo) {
+    const uint32_t pos = chunk * ch + (__ffs(todo) - 1u);
+    todo &= todo - 1u;
+    const uint32_t e = P.large_ids[pos];
     uint64_t b;
     uint32_t s;
     P.csr.range(e, b, s);
     const uint32_t* __restrict__ pp = P.csr.pins + b;
-    bool dead_any = false;
-    if (r > 1)
-      for (uint32_t i = lane; i < s; i += 32) dead_any |= (__ldcg(P.vtop + __ldg(pp + i)) == kTopDead);
-    dead_any = __any_sync(0xffffffffu, dead_any);
+    unsigned long long key = 0ull;
+    if constexpr (VMAX) key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
+    const uint32_t hi = static_cast<uint32_t>(key >> 32);
+    bool dead_any = false, lost = false;
+    // pass 1: filter words of all pins (32 gathers in flight per step)
+    for (uint32_t i0 = 0; i0 < s && !dead_any; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t cur = i < s ? __ldcg(P.vtop + __ldg(pp + i)) : 0u;
+      dead_any = __any_sync(0xffffffffu, r > 1 && cur == kTopDead);
+      lost |= cur > hi;
+    }
     if (dead_any) {
-      local_deact += (lane == 0);
+      if (lane == 0) {
+        P.large_state[pos] = LARGE_DROPPED;
+        ++local_deact;
+      }
       continue;
     }
-    if (lane == 0) out[atomicAdd(&c->count1[par ^ 1], 1u)] = e;
+    local_alive += (lane == 0);
     if constexpr (VMAX) {
-      const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
         tie |= deposit_key(P, v, key, __ldcg(P.vtop + v));
       }
+      lost = __any_sync(0xffffffffu, lost);
+      if (lane == 0) P.large_state[pos] = lost ? LARGE_ACTIVE : LARGE_CANDIDATE;
     }
+   }
   }
   if (local_deact) atomicAdd(P.deact_cnt + (r - 1), local_deact);
+  if (local_alive) atomicAdd(&c->count1[par ^ 1], local_alive);
   if (tie) c->tie_flag = 1u;
 }
 
@@ -673,16 +698,20 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
   const Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
-  const uint32_t par = c->parity;
-  const uint32_t cnt = c->count1[par ^ 1];
-  const uint32_t* __restrict__ list = P.list1[par ^ 1];
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
   uint32_t local_matched = 0;
-  for (uint32_t pos = warp; pos < cnt; pos += nwarps) {
-    const uint32_t e = list[pos];
+  const uint32_t ch = P.large_chunk;
+  for (uint32_t chunk = warp; static_cast<uint64_t>(chunk) * ch < P.num_large; chunk += nwarps) {
+   const uint32_t my_pos = chunk * ch + lane;
+   uint32_t todo = __ballot_sync(0xffffffffu,
+                                 lane < ch && my_pos < P.num_large && P.large_state[my_pos] == LARGE_CANDIDATE);
+   while (todo) {
+    const uint32_t pos = chunk * ch + (__ffs(todo) - 1u);
+    todo &= todo - 1u;
+    const uint32_t e = P.large_ids[pos];
     uint64_t b;
     uint32_t s;
     P.csr.range(e, b, s);
@@ -705,6 +734,7 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
         ++local_matched;
       }
     }
+   }
   }
   if (local_matched) atomicAdd(P.matched_cnt + r, local_matched);
 }
@@ -757,10 +787,9 @@ struct ExactParams {
   unsigned long long* vb;  // n: max tie hash among weight maxima
   uint32_t* vc;            // n: max (global id + 1) among (weight, hash) maxima
   uint32_t round;
-  uint32_t cls;            // 0: segmented lists of buffer `buf`; 1: appended list of large edges
+  uint32_t cls;            // 0: segmented lists of buffer `buf`; 1: the large edges (state bytes)
   uint32_t buf;
   uint32_t ident;          // class 0 only: the list is the identity
-  uint32_t count1;         // class 1 length
 };
 
 template <int LEVEL>
@@ -769,7 +798,7 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
   const uint64_t warp = blockIdx.x * static_cast<uint64_t>(kWarpsPerBlock) + (threadIdx.x >> 5);
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
   const uint32_t r = X.round;
-  const uint64_t slots = X.cls == 0 ? static_cast<uint64_t>(P.nseg) * P.seg_cap : X.count1;
+  const uint64_t slots = X.cls == 0 ? static_cast<uint64_t>(P.nseg) * P.seg_cap : P.num_large;
   uint32_t local_matched = 0;
   for (uint64_t pos = warp; pos < slots; pos += nwarps) {
     uint32_t e;
@@ -779,7 +808,8 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
       if (idx >= region_count(P, X.ident, P.seg_cnt[X.buf], seg)) continue;
       e = X.ident ? static_cast<uint32_t>(pos) : P.seg_ids[X.buf][pos];
     } else {
-      e = P.list1[X.buf][pos];
+      if (P.large_state[pos] == LARGE_DROPPED) continue;
+      e = P.large_ids[pos];
     }
     uint64_t b;
     uint32_t s;
@@ -1126,8 +1156,8 @@ __global__ void __launch_bounds__(kBlock) k_mg_claims(const RoundParams P, uint3
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
-  const uint32_t cnt1 = c->count1[par ^ 1];
-  for (uint32_t pos = warp; pos < cnt1; pos += nwarps) mg_claim_edge(P, P.list1[par ^ 1][pos], r, tag, claims, lane, 32);
+  for (uint32_t pos = warp; pos < P.num_large; pos += nwarps)
+    if (P.large_state[pos] != LARGE_DROPPED) mg_claim_edge(P, P.large_ids[pos], r, tag, claims, lane, 32);
 }
 
 // any vertex claimed twice?  (a nibble >= 2 has one of its three upper bits set)

@@ -18,7 +18,7 @@
 // space is cut into nseg regions of seg_cap ids; a CTA claims a region by ticket, filters it and
 // writes the survivors back into the same region of the other buffer.  No global scan, no
 // contended append counter, and the lists stay in ascending-id order (deterministic content,
-// monotone pin addresses).  Class 1 (larger edges, one warp per edge) is a plain appended list.
+// monotone pin addresses).  Class 1 (larger edges, one warp per edge) keeps a state byte per edge.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -46,7 +46,7 @@ struct Ctrl {
   uint32_t ticket_f;     // region tickets of the filter kernel
   uint32_t ticket_c;     // region tickets of the check kernel
   uint32_t active_small; // class-0 edges active in this round (sum of region counts)
-  uint32_t count1[2];    // [buffer] class-1 list lengths
+  uint32_t count1[2];    // [buffer] active class-1 (large) edges
   uint32_t tie_flag;
   uint32_t status;
   uint32_t max_rounds;
@@ -102,8 +102,11 @@ struct RoundParams {
   uint32_t check_claim;      // regions a warp of the check kernel claims per ticket (1..8)
   uint32_t* cand_ids;        // class 0, same regions: edges that did not lose during vertex-max
   uint32_t* cand_cnt;        // [nseg]
-  // class 1: appended list
-  uint32_t* list1[2];
+  // class 1: the (static) list of large edges and a state byte per entry
+  const uint32_t* large_ids;
+  uint8_t* large_state;
+  uint32_t num_large;
+  uint32_t large_chunk;      // entries of the large list a warp scans per step (power of two, 1..32)
   uint32_t* matched_cnt;     // [round] edges matched in that round
   uint32_t* deact_cnt;       // [round] edges dropped after that round (matched + deactivated)
 };
