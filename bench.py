@@ -12,8 +12,10 @@ rounds, result assembled and copied back) of the workload instance.
                   timed with CUDA events on the launching stream around exactly K steps.
 * e2e          -- the same metric through the drop-in call hlm_b200_match_host (C-ABI, host
                   buffers): H2D of the CSR from pinned memory, loader kernels, matching, result D2H.
-* roofline     -- dominant kernel (k_filter_vmax) algorithmic bytes / its CUDA-event time vs the
-                  measured HBM copy bandwidth (MEASURED_PEAKS.json).
+* roofline     -- dominant kernel (the round sweep: k_sweep_uniform in round 1, k_sweep_uniform_simple
+                  afterwards) algorithmic bytes / its CUDA-event time vs the measured HBM copy
+                  bandwidth (MEASURED_PEAKS.json); `traffic` = DRAM bytes per launch from the ncu
+                  capture of the same workload (profiles/traffic_r01.json).
 * cpu_baseline -- the unmodified reference (oracle/_ref) on a bounded sample of the workload,
                   timed on this box's host cores.
 
@@ -305,7 +307,9 @@ def main():
     filt_total_ms, chk_total_ms = float(filt_ms.sum()), float(chk_ms.sum())
     n_launch = len(fb)
     achieved = sum(fb) / (filt_total_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_filter_vmax_small (invalidate + compact + vertex-max atomics)",
+    roofline = {"bound": "hbm",
+                "kernel": "round sweep: k_sweep_uniform<2,1,1> (round 1) + k_sweep_uniform_simple<2,1> (later rounds): "
+                          "invalidate + compact + key + vertex-max atomics",
                 "achieved": achieved, "peak": hbm_gbs, "peak_source": peak_src, "unit": "GB/s",
                 "frac": achieved / hbm_gbs, "traffic": None,
                 "launches_per_step": n_launch, "algorithmic_bytes_per_launch": sum(fb) / n_launch,
@@ -314,6 +318,8 @@ def main():
                 "round1_frac": fb[0] / (float(filt_ms[0]) * 1e-3) / 1e9 / hbm_gbs,
                 "check_kernel": {"achieved": sum(cb) / (chk_total_ms * 1e-3) / 1e9,
                                  "frac": sum(cb) / (chk_total_ms * 1e-3) / 1e9 / hbm_gbs},
+                "note": "the sweeps are bound by the SM's sector rate for uncoalesced accesses (1 sector/clk/SM = "
+                        "285-300 G random 4-byte gathers/s measured, scripts/micro/gather_bench.cu), not by HBM",
                 "whole_job": {"algorithmic_bytes": total_bytes, "achieved": total_bytes / (ms_per_step * 1e-3) / 1e9,
                               "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_gbs}}
     traffic_file = os.path.join(ROOT, "profiles", "traffic_r01.json")

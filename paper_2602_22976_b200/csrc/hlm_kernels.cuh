@@ -311,11 +311,16 @@ __global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundP
         e = in_ident ? seg_base + idx : __ldcs(in + seg_base + idx);
         pv = load_pins_stream<D>(P.csr.pins, e);
         if (peek) {
+          // first pin first (coalesced: the edges are sorted by it); about half of the edges that
+          // die are already decided here and never issue the random gathers of their other pins
+          cur[0] = HLM_VTOP_LD(P.vtop + pv.v[0]);
+          bool dead_any = cur[0] == kTopDead;
+          if (!dead_any) {
 #pragma unroll
-          for (int i = 0; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
-          bool dead_any = false;
+            for (int i = 1; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
 #pragma unroll
-          for (int i = 0; i < D; ++i) dead_any |= (cur[i] == kTopDead);
+            for (int i = 1; i < D; ++i) dead_any |= (cur[i] == kTopDead);
+          }
           if (dead_any) {
             survive = false;
             ++local_deact;
@@ -1143,7 +1148,7 @@ __device__ __forceinline__ void mg_claim_edge(const RoundParams& P, uint32_t e, 
 // every local edge that holds the (global) maximum at one of its pins claims that vertex
 __global__ void __launch_bounds__(kBlock) k_mg_claims(const RoundParams P, uint32_t* claims) {
   const Ctrl* c = P.ctrl;
-  const uint32_t r = c->round, par = c->parity;
+  const uint32_t r = c->round;
   const uint32_t tag = round_tag(P.ks, r);
   const uint64_t slots = static_cast<uint64_t>(P.nseg) * P.seg_cap;
   for (uint64_t pos = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; pos < slots;
