@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HLM_B200_ABI_VERSION 1
+#define HLM_B200_ABI_VERSION 2
 
 typedef enum {
   HLM_B200_OK = 0,
@@ -36,7 +36,11 @@ typedef enum {
 enum { HLM_B200_GEN_XORSHIFT = 0, HLM_B200_GEN_PARK_MILLER = 1, HLM_B200_GEN_SPLITMIX = 2 };
 enum { HLM_B200_MODE_PERTURB_BASE = 0, HLM_B200_MODE_REPLACE_UNIFORM = 1 };
 
-/* hlm::Variant (local_max_par.hpp:34), same enumerator order.  Implemented: CRCW, CREW. */
+/* hlm::Variant (local_max_par.hpp:34), same enumerator order.  CRCW and CREW have their own device
+ * kernels.  SEQ and WORK_OPTIMAL are accepted and executed by the CRCW kernels (all variants return
+ * the same matching by contract, tests/test_par.cpp:32-55; the CRCW path already compacts its
+ * active lists every round, which is what work_optimal is for); their WorkCounters follow the
+ * reference's own per-variant formulas.  GREEDY (a different, sequential algorithm) is not. */
 enum {
   HLM_B200_VARIANT_SEQ = 0,
   HLM_B200_VARIANT_CRCW = 1,
@@ -97,7 +101,7 @@ typedef struct {
   uint64_t total_edge_visits;      /* WorkCounters by the reference's per-variant formulas */
   uint64_t total_pin_visits;
   uint64_t device_edge_visits;     /* what the device really swept: sum over rounds of m_r */
-  uint64_t device_pin_visits;      /* sum over rounds of kappa_r (only counted when cheap; else 0) */
+  uint64_t device_pin_visits;      /* sum over rounds of kappa_r (pins of the edges active in round r) */
   double wall_time_ms;             /* host clock around the matching (upload excluded) */
   double device_ms;                /* CUDA events around the round loop + result assembly */
   uint32_t tie_redo_rounds;        /* rounds that were redone on the exact three-level path */
@@ -109,6 +113,8 @@ typedef struct {
   float* round_filter_ms;
   float* round_check_ms;
   uint64_t h2d_bytes;              /* hlm_b200_match_host: bytes the loader moved host -> device */
+  uint32_t prefix_sum_invocations; /* WorkCounters (matching.hpp:27-33): non-zero for WORK_OPTIMAL only */
+  uint32_t compactions;
 } hlm_b200_result;
 
 typedef struct hlm_b200_graph hlm_b200_graph; /* opaque: instance resident in HBM */

@@ -88,6 +88,8 @@ inline MatchResult take(hlm_b200_result& r) {
   rep.work.rounds = r.rounds;
   rep.work.total_edge_visits = r.total_edge_visits;
   rep.work.total_pin_visits = r.total_pin_visits;
+  rep.work.prefix_sum_invocations = r.prefix_sum_invocations;
+  rep.work.compactions = r.compactions;
   rep.wall_time_ms = r.wall_time_ms;
   rep.write_conflicts = r.write_conflicts;
   hlm_b200_result_free(&r);

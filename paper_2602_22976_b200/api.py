@@ -207,7 +207,8 @@ def _convert(status: int, res: _lib.Result) -> MatchResult:
     prd = _take(res.per_round_deactivated, res.rounds, np.uint32).tolist()
     matching = Matching(matched, float(res.total_weight), int(res.rounds), prm)
     report = RunReport(int(res.rounds), prm, prd, round_of,
-                       WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits)),
+                       WorkCounters(int(res.rounds), int(res.total_edge_visits), int(res.total_pin_visits),
+                                    int(res.prefix_sum_invocations), int(res.compactions)),
                        float(res.wall_time_ms), int(res.write_conflicts), float(res.device_ms),
                        int(res.device_edge_visits), int(res.tie_redo_rounds), int(res.kernel_launches),
                        int(res.graph_launches), matched,

@@ -1060,6 +1060,8 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   out->tie_redo_rounds = tie_redo;
   out->graph_launches = graph_launches;
   out->device_edge_visits = c.edges_swept;
+  out->device_pin_visits = c.pins_swept;
+  g->ws.pins_matched = c.pins_matched;
   // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
   out->kernel_launches = L.launches + graph_kernels;
   for (auto& ev : tev)
@@ -1072,7 +1074,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
       out->round_check_ms[i] = t_check[i];
     }
   }
-  int rc = assemble_result(g, rounds, cfg, HLM_B200_VARIANT_CRCW, out);
+  int rc = assemble_result(g, rounds, cfg, cfg->variant, out);
   if (rc != HLM_B200_OK) return rc;
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
@@ -1174,13 +1176,25 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     }
   }
   out->total_weight = tw;
-  // WorkCounters by the reference's formulas (local_max_par.hpp:135,159,164,224,248 for crcw;
-  // :135,159,164,285,299,320-321 for crew): soft-deletion variants charge the full structure
-  // every round.
-  const uint64_t per_round_edges = variant == HLM_B200_VARIANT_CREW ? 5ull : 3ull;
-  const uint64_t per_round_pins = variant == HLM_B200_VARIANT_CREW ? 4ull : 3ull;
-  out->total_edge_visits = per_round_edges * m * rounds;
-  out->total_pin_visits = per_round_pins * g->kappa * rounds;
+  // WorkCounters by the reference's per-variant formulas.  Soft-deletion variants charge the full
+  // structure every round: seq 3m / 3k (local_max_seq.hpp:45-48,104), crcw 3m / 3k
+  // (local_max_par.hpp:135,159,164,224,248), crew 5m / 4k (:135,159,164,285,299,320-321).
+  // work_optimal charges what is left: per round 3 m_r + m_r edge visits (:496,528,547; compact :453)
+  // and 3 k_r + matched pins (:557) + 2 k_r + 3 k_{r+1} pin visits (compact :452), four scans and
+  // one compaction.  sum m_r and sum k_r come from the device (Ctrl::edges_swept / pins_swept).
+  if (variant == HLM_B200_VARIANT_WORK_OPTIMAL) {
+    const uint64_t sum_m = out->device_edge_visits, sum_k = out->device_pin_visits;
+    const uint64_t matched_pins = g->uniform_d ? static_cast<uint64_t>(g->uniform_d) * total : w.pins_matched;
+    out->total_edge_visits = 4ull * sum_m;
+    out->total_pin_visits = 5ull * sum_k + matched_pins + 3ull * (sum_k >= g->kappa ? sum_k - g->kappa : 0ull);
+    out->prefix_sum_invocations = 4u * rounds;
+    out->compactions = rounds;
+  } else {
+    const uint64_t per_round_edges = variant == HLM_B200_VARIANT_CREW ? 5ull : 3ull;
+    const uint64_t per_round_pins = variant == HLM_B200_VARIANT_CREW ? 4ull : 3ull;
+    out->total_edge_visits = per_round_edges * m * rounds;
+    out->total_pin_visits = per_round_pins * g->kappa * rounds;
+  }
   out->write_conflicts = 0;
   return HLM_B200_OK;
 }
@@ -1205,15 +1219,15 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
   int rc;
   switch (cfg->variant) {
     case HLM_B200_VARIANT_CRCW:
+    case HLM_B200_VARIANT_SEQ:           // same matching by contract; executed by the CRCW kernels,
+    case HLM_B200_VARIANT_WORK_OPTIMAL:  // WorkCounters by the variant's own formulas
       rc = match_crcw(g, st, cfg, out);
       break;
     case HLM_B200_VARIANT_CREW:
       rc = match_crew(g, st, cfg, out);
       break;
-    case HLM_B200_VARIANT_SEQ:
-    case HLM_B200_VARIANT_WORK_OPTIMAL:
     case HLM_B200_VARIANT_GREEDY:
-      set_error("variant %d is not implemented on the device (crcw = 1 and crew = 2 are)", cfg->variant);
+      set_error("variant greedy (a sequential baseline, local_max_seq.hpp:130) is not implemented on the device");
       return HLM_B200_ERR_UNSUPPORTED;
     default:
       set_error("unknown variant %d", cfg->variant);  // local_max_par.hpp:615

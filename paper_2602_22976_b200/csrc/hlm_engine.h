@@ -53,6 +53,7 @@ struct Workspace {
   uint32_t graph_head_launches = 0;  // round 1 (ahead of the WHILE node)
   uint32_t graph_body_launches = 0;  // one iteration of the WHILE body
   uint32_t launches = 0;
+  unsigned long long pins_matched = 0;  // ragged instances: pins of the matched edges of the last run
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void drop_graphs();
   void release();

@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t local_deact = 0, local_kept = 0;
+  unsigned long long local_pins = 0;  // pins of the edges this thread keeps (WorkCounters of work_optimal)
   bool tie = false;
 
   const uint32_t gran = claim_granularity(P, c->active_prev);
@@ -405,10 +406,12 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
       bool is_long = false;
       uint64_t long_b = 0;
       uint32_t long_s = 0;
+      uint32_t my_size = 0;
       if (survive) {
         uint64_t b;
         uint32_t s;
         P.csr.range(e, b, s);
+        my_size = s;
         if (P.has_large && s > kLargeEdge) {
           survive = false;  // class-1 edge seen through the identity list
         } else {
@@ -479,10 +482,12 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
           }
         }
       }
-      if (!out_ident) {
-        // order-preserving warp compaction
+      if (survive) local_pins += my_size;
+      {
+        // order-preserving warp compaction (round 1 keeps the identity list and only counts: the
+        // large edges seen through it belong to class 1 and must not be counted here)
         const uint32_t ballot = __ballot_sync(0xffffffffu, survive);
-        if (survive) out[seg_base + out_off + __popc(ballot & lt_mask)] = e;
+        if (survive && !out_ident) out[seg_base + out_off + __popc(ballot & lt_mask)] = e;
         out_off += __popc(ballot);
       }
       if constexpr (VMAX) {
@@ -493,16 +498,17 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
       }
     }
     if (lane == 0) {
-      const uint32_t kept = out_ident ? cnt : out_off;
-      out_cnt[seg] = kept;
+      out_cnt[seg] = out_ident ? cnt : out_off;  // list length (round 2 reads the identity list anyway)
       if (VMAX) P.cand_cnt[seg] = cand_off;
-      local_kept += kept;
+      local_kept += out_off;
     }
   }
   const uint32_t d = warp_sum(local_deact);
+  for (int o = 16; o > 0; o >>= 1) local_pins += __shfl_xor_sync(0xffffffffu, local_pins, o);
   if (lane == 0) {
     if (d) atomicAdd(P.deact_cnt + (r - 1), d);
     if (local_kept) atomicAdd(&c->active_small, local_kept);
+    if (local_pins) atomicAdd(&c->pins_round, local_pins);
   }
   if (tie) c->tie_flag = 1u;
 }
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   const uint32_t* __restrict__ list_cnt = P.cand_cnt;
   const uint32_t tag = round_tag(P.ks, r);
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t local_matched = 0;
+  uint32_t local_matched = 0, local_mpins = 0;
 
   for (;;) {
     const uint32_t seg0 = claim_region(&c->ticket_c, lane) * P.check_claim;
@@ -620,6 +626,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
                 mark_dead(P, v);
               }
               ++local_matched;
+              local_mpins += s;
             }
           }
         }
@@ -628,6 +635,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   }
   const uint32_t t = warp_sum(local_matched);
   if (lane == 0 && t) atomicAdd(P.matched_cnt + r, t);
+  if constexpr (D == 0) {
+    const uint32_t mp = warp_sum(local_mpins);  // a warp matches far fewer than 2^32 pins per launch
+    if (lane == 0 && mp) atomicAdd(&c->pins_matched, static_cast<unsigned long long>(mp));
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -649,6 +660,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
   uint32_t local_deact = 0, local_alive = 0;
+  unsigned long long local_pins = 0;
   bool tie = false;
   // a warp takes 32 consecutive entries: one coalesced load of their state bytes, then the active
   // ones in turn, each with all 32 lanes
@@ -683,7 +695,10 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
       }
       continue;
     }
-    local_alive += (lane == 0);
+    if (lane == 0) {
+      ++local_alive;
+      local_pins += s;
+    }
     if constexpr (VMAX) {
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
@@ -696,6 +711,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   }
   if (local_deact) atomicAdd(P.deact_cnt + (r - 1), local_deact);
   if (local_alive) atomicAdd(&c->count1[par ^ 1], local_alive);
+  if (local_pins) atomicAdd(&c->pins_round, local_pins);
   if (tie) c->tie_flag = 1u;
 }
 
@@ -708,6 +724,7 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
   const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
   uint32_t local_matched = 0;
+  unsigned long long local_mpins = 0;
   const uint32_t ch = P.large_chunk;
   for (uint32_t chunk = warp; static_cast<uint64_t>(chunk) * ch < P.num_large; chunk += nwarps) {
    const uint32_t my_pos = chunk * ch + lane;
@@ -737,11 +754,13 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
       if (lane == 0) {
         mark_matched(P, e, r);
         ++local_matched;
+        local_mpins += s;
       }
     }
    }
   }
   if (local_matched) atomicAdd(P.matched_cnt + r, local_matched);
+  if (local_mpins) atomicAdd(&P.ctrl->pins_matched, local_mpins);
 }
 
 // One thread.  Round bookkeeping between check/commit of round r and the filter of round r+1;
@@ -764,6 +783,9 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
     c->rounds_done = r - 1;
   } else {
     c->edges_swept += active;
+    // uniform instances: kappa_r = d * m_r; ragged ones: counted by the sweeps of this round
+    c->pins_swept += P.csr.uniform_d ? static_cast<unsigned long long>(active) * P.csr.uniform_d : c->pins_round;
+    c->pins_round = 0;
     c->active_prev = c->active_small;
     c->active_small = 0;
     c->parity = par ^ 1;
@@ -805,6 +827,7 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
   const uint32_t r = X.round;
   const uint64_t slots = X.cls == 0 ? static_cast<uint64_t>(P.nseg) * P.seg_cap : P.num_large;
   uint32_t local_matched = 0;
+  unsigned long long local_mpins = 0;
   for (uint64_t pos = warp; pos < slots; pos += nwarps) {
     uint32_t e;
     if (X.cls == 0) {
@@ -850,11 +873,13 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
         if (lane == 0) {
           mark_matched(P, e, r);
           ++local_matched;
+          local_mpins += s;
         }
       }
       }
   }
   if (LEVEL == 4 && local_matched) atomicAdd(P.matched_cnt + r, local_matched);
+  if (LEVEL == 4 && local_mpins) atomicAdd(&P.ctrl->pins_matched, local_mpins);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -52,7 +52,10 @@ struct Ctrl {
   uint32_t max_rounds;
   uint32_t rounds_done;
   uint32_t active_prev;  // class-0 edges in the list the next sweep reads (0 before round 2)
-  unsigned long long edges_swept;  // sum over rounds of the active-list lengths
+  unsigned long long edges_swept;  // sum over rounds of the active-list lengths (sum of m_r)
+  unsigned long long pins_swept;   // sum over rounds of the pins of the active edges (sum of kappa_r)
+  unsigned long long pins_round;   // ragged instances: pins of the edges kept by this round's sweeps
+  unsigned long long pins_matched; // ragged instances: pins of all matched edges so far
 };
 
 struct EdgeCsr {

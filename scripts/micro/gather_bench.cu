@@ -55,8 +55,8 @@ void run(const char* name, const uint32_t* table, uint32_t entries, const uint32
     if (ms < best) best = ms;
   }
   const double n = (double)per_thread * grid * 256;
-  printf("%-10s table %4u MB  ilp %d  ctas/sm %d : %.3f ms  %.1f G gathers/s  (%.2f sectors/clk/SM at 1.92 GHz)\n", name,
-         entries / (1u << 18), ILP, blocks_per_sm, best, n / best / 1e6, n / best / 1e6 / 1.92 / sms);
+  printf("%-10s table %7u KB  ilp %d  ctas/sm %d : %.3f ms  %.1f G gathers/s  (%.2f sectors/clk/SM at 1.92 GHz)\n", name,
+         entries / (1u << 8), ILP, blocks_per_sm, best, n / best / 1e6, n / best / 1e6 / 1.92 / sms);
 }
 
 int main() {
@@ -67,7 +67,7 @@ int main() {
   cudaMalloc(&idx, (size_t)(1ull << 29) * 4 + (1 << 20));
   cudaMemset(idx, 0x5a, (size_t)(1ull << 29) * 4);
   cudaMalloc(&out, 4);
-  for (uint32_t lg : {19u, 24u, 27u, 28u}) {  // 2 MB, 64 MB, 512 MB, 1 GB
+  for (uint32_t lg : {13u, 14u, 15u, 16u, 17u, 19u, 24u, 27u, 28u}) {  // 32 KB .. 512 KB (L1), 2 MB, 64 MB (L2), 512 MB, 1 GB (HBM)
     const uint32_t entries = 1u << lg;
     run<1, 0>("ld.ca", table, entries, idx, out, 8);
     run<4, 0>("ld.ca", table, entries, idx, out, 8);

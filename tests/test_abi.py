@@ -26,7 +26,7 @@ def test_header_symbols_are_exported(hb):
         assert hasattr(lib, name), f"{name} declared in include/hlm_b200.h but not exported"
     # the Python binding covers the same set
     assert sorted(_lib.SYMBOLS) == declared
-    assert lib.hlm_b200_abi_version() == 1
+    assert lib.hlm_b200_abi_version() == 2
 
 
 def test_struct_layouts_match_the_header(hb, tmp_path):
