@@ -116,7 +116,7 @@ template <int D, bool VMAX, bool R1, int NPEND>
 struct SweepCtx {
   const RoundParams& P;
   uint32_t r, tag, lane, lt_mask;
-  bool in_ident, out_ident, peek;
+  bool in_ident, out_ident, peek, dead_first;
   const uint32_t* __restrict__ in;
   uint32_t* __restrict__ out;
   uint32_t seg_base, cnt;
@@ -128,8 +128,13 @@ struct SweepCtx {
 #pragma unroll
     for (int i = 0; i < D; ++i) b.cur[i] = 0u;
     if (peek && b.live) {
+      if (dead_first) {
 #pragma unroll
-      for (int i = 0; i < D; ++i) b.cur[i] = HLM_VTOP_LD(P.vtop + b.pv.v[i]);
+        for (int i = 0; i < D; ++i) b.cur[i] = dead_word(P.dead_all, b.pv.v[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i) b.cur[i] = HLM_VTOP_LD(P.vtop + b.pv.v[i]);
+      }
     }
     // ---- stage A: ids and pins of batch it
     {
@@ -163,6 +168,10 @@ struct SweepCtx {
       if (VMAX && c1.live) {
         c1.oid = P.orig ? __ldg(P.orig + c1.e) : c1.e;
         c1.base = base_of(P, c1.e);
+        if (dead_first) {  // only the survivors pay for the (HBM-resident) filter words
+#pragma unroll
+          for (int i = 0; i < D; ++i) c1.cur[i] = HLM_VTOP_LD(P.vtop + c1.pv.v[i]);
+        }
       }
     }
     // ---- stage C2: batch it-3
@@ -220,6 +229,7 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   X.in_ident = R1 || X.r <= 2;   // rounds 1 and 2 read the identity list
   X.out_ident = R1 || X.r == 1;  // round 1 keeps every edge: nothing to write
   X.peek = X.r > 1 || P.ks.precheck;
+  X.dead_first = !R1 && X.r > 1 && P.dead_first;
   X.in = P.seg_ids[par];
   X.out = P.seg_ids[par ^ 1];
   const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
@@ -280,6 +290,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundP
   const bool in_ident = r <= 2;
   const bool out_ident = r == 1;
   const bool peek = r > 1 || P.ks.precheck;
+  const bool dead_first = r > 1 && P.dead_first;
   const uint32_t* __restrict__ in = P.seg_ids[par];
   const uint32_t* __restrict__ in_cnt = P.seg_cnt[par];
   uint32_t* __restrict__ out = P.seg_ids[par ^ 1];
@@ -313,13 +324,23 @@ __global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundP
         if (peek) {
           // first pin first (coalesced: the edges are sorted by it); about half of the edges that
           // die are already decided here and never issue the random gathers of their other pins
-          cur[0] = HLM_VTOP_LD(P.vtop + pv.v[0]);
-          bool dead_any = cur[0] == kTopDead;
-          if (!dead_any) {
+          bool dead_any = false;
+          if (dead_first) {
 #pragma unroll
-            for (int i = 1; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+            for (int i = 0; i < D; ++i) dead_any |= vertex_dead(P.dead_all, pv.v[i]);
+            if (VMAX && !dead_any) {
 #pragma unroll
-            for (int i = 1; i < D; ++i) dead_any |= (cur[i] == kTopDead);
+              for (int i = 0; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+            }
+          } else {
+            cur[0] = HLM_VTOP_LD(P.vtop + pv.v[0]);
+            dead_any = cur[0] == kTopDead;
+            if (!dead_any) {
+#pragma unroll
+              for (int i = 1; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+#pragma unroll
+              for (int i = 1; i < D; ++i) dead_any |= (cur[i] == kTopDead);
+            }
           }
           if (dead_any) {
             survive = false;
@@ -387,6 +408,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
   uint32_t local_deact = 0, local_kept = 0;
   unsigned long long local_pins = 0;  // pins of the edges this thread keeps (WorkCounters of work_optimal)
   bool tie = false;
+  const bool dead_first = r > 1 && P.dead_first;
 
   const uint32_t gran = claim_granularity(P, c->active_prev);
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
@@ -422,10 +444,14 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
             uint32_t v[8], cur[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[i] = static_cast<uint32_t>(i) < s ? __ldg(pp + i) : 0u;
+            bool dead_any = false;
+            if (dead_first) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && vertex_dead(P.dead_all, v[i]));
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              cur[i] = (peek && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
-            bool dead_any = false;
+              cur[i] = (peek && !dead_any && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
             if (dead_any) {
@@ -463,8 +489,9 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
         const bool mine = lane < es;
         const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
         const bool peek = r > 1 || P.ks.precheck;
-        const uint32_t cur = (mine && peek) ? HLM_VTOP_LD(P.vtop + v) : 0u;
-        const bool dead_any = __any_sync(0xffffffffu, mine && cur == kTopDead);
+        bool dead_any = dead_first && __any_sync(0xffffffffu, mine && vertex_dead(P.dead_all, v));
+        const uint32_t cur = (mine && peek && !dead_any) ? HLM_VTOP_LD(P.vtop + v) : 0u;
+        dead_any = dead_any || __any_sync(0xffffffffu, mine && cur == kTopDead);
         bool lost = false;
         if (!dead_any) {
           if constexpr (VMAX) {
@@ -681,12 +708,18 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
     if constexpr (VMAX) key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
     const uint32_t hi = static_cast<uint32_t>(key >> 32);
     bool dead_any = false, lost = false;
-    // pass 1: filter words of all pins (32 gathers in flight per step)
-    for (uint32_t i0 = 0; i0 < s && !dead_any; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t cur = i < s ? __ldcg(P.vtop + __ldg(pp + i)) : 0u;
-      dead_any = __any_sync(0xffffffffu, r > 1 && cur == kTopDead);
-      lost |= cur > hi;
+    // pass 1: is a pin dead?  (32 gathers in flight per step; the bitmap when vtop is HBM-resident)
+    if (r > 1) {
+      const bool use_bits = P.dead_first != 0u;
+      for (uint32_t i0 = 0; i0 < s && !dead_any; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool d = false;
+        if (i < s) {
+          const uint32_t v = __ldg(pp + i);
+          d = use_bits ? vertex_dead(P.dead_all, v) : (__ldcg(P.vtop + v) == kTopDead);
+        }
+        dead_any = __any_sync(0xffffffffu, d);
+      }
     }
     if (dead_any) {
       if (lane == 0) {
@@ -702,7 +735,9 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
     if constexpr (VMAX) {
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
-        tie |= deposit_key(P, v, key, __ldcg(P.vtop + v));
+        const uint32_t cur = __ldcg(P.vtop + v);
+        tie |= deposit_key(P, v, key, cur);
+        lost |= cur > hi;
       }
       lost = __any_sync(0xffffffffu, lost);
       if (lane == 0) P.large_state[pos] = lost ? LARGE_ACTIVE : LARGE_CANDIDATE;
@@ -1199,9 +1234,11 @@ __global__ void k_mg_tie_scan(const uint32_t* claims, uint64_t words, uint32_t* 
   if (any) *flag = 1u;
 }
 
-__global__ void k_mg_apply_dead(const uint32_t* dead_new, uint32_t words, uint32_t* vtop, uint32_t n) {
+__global__ void k_mg_apply_dead(const uint32_t* dead_new, uint32_t words, uint32_t* vtop, uint32_t n,
+                                uint32_t* dead_all) {
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
     uint32_t bits = dead_new[w];
+    if (bits) dead_all[w] |= bits;
     while (bits) {
       const uint32_t v = w * 32u + (__ffs(bits) - 1u);
       bits &= bits - 1u;

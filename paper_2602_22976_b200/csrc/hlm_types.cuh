@@ -94,7 +94,10 @@ struct RoundParams {
   Ctrl* ctrl;
   unsigned long long* vkey;  // n round-tagged vertex maxima (full 64-bit keys)
   uint32_t* vtop;            // n: high word of vkey, or kTopDead; the L2-resident filter array
-  uint32_t* dead;            // n bits: vertex covered by a matched edge
+  uint32_t* dead;            // n bits: where completion marking sets its bits (multi-GPU: the exchange area)
+  const uint32_t* dead_all;  // n bits: every vertex covered so far; stable during a sweep
+  uint32_t dead_first;       // sweeps of rounds >= 2 test the bitmap (n/8 bytes, L2-resident) before
+                             // they touch vtop
   uint32_t* mbits;           // m bits: edge matched
   uint16_t* mround;          // m: round an edge matched in (valid where its mbits bit is set)
   // class 0: segmented lists
@@ -126,6 +129,11 @@ constexpr uint32_t kTopDead = 0xFFFFFFFFu;
 
 __device__ __forceinline__ bool vertex_dead(const uint32_t* dead, uint32_t v) {
   return (__ldg(dead + (v >> 5)) >> (v & 31)) & 1u;
+}
+// kTopDead if v was covered in an earlier round, else 0: a stand-in for vtop[v] that only answers
+// the deactivation question (rounds >= 2 of instances whose vtop does not fit in L2)
+__device__ __forceinline__ uint32_t dead_word(const uint32_t* dead_all, uint32_t v) {
+  return vertex_dead(dead_all, v) ? 0xFFFFFFFFu : 0u;
 }
 
 // The id the reference knows an edge by: keys, tie hashes and results always use it.
