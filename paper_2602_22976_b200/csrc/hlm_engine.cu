@@ -398,6 +398,20 @@ int new_graph(int device, Graph** out) {
 // uniformity and pack the weights to one byte each; what passes is not uploaded (offsets) or
 // uploaded packed and widened on the device (weights).  Anything else takes the plain path.
 // ---------------------------------------------------------------------------------------------
+// HLM_B200_TRACE=1: phase times of the loader / one-shot call on stderr
+struct PhaseTrace {
+  bool on = std::getenv("HLM_B200_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hlm_b200] %-28s %8.2f ms  (+%.2f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - t0).count(),
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
+
 struct UploadPlan {
   bool reorder = true;      // sort the resident edges by first pin (pays off after ~30 matchings)
   bool host_assist = true;  // use the host cores as described above
@@ -414,31 +428,40 @@ struct HostScan {
   std::atomic<bool> nopack{false};
   static constexpr uint64_t kChunk = 1ull << 20;
   uint64_t chunks_per_array() const { return (m + kChunk - 1) / kChunk; }
-  void work() {
+  std::atomic<uint64_t> weight_chunks_done{0};
+  // Weight chunks come first in the queue: the packed bytes are ready well before the pins have
+  // crossed PCIe, so their upload (queued by `on_weights_ready`, main thread only) hides behind
+  // the scan of the offsets.
+  template <typename F>
+  void work(F&& on_weights_ready) {
     const uint64_t nc = chunks_per_array();
     for (;;) {
+      on_weights_ready();
       const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
-      if (t >= 2 * nc) return;
-      const bool is_off = t < nc;
-      const uint64_t b = (is_off ? t : t - nc) * kChunk, e = std::min(m, b + kChunk);
+      if (t >= 2 * nc) break;
+      const bool is_off = t >= nc;
+      const uint64_t b = (is_off ? t - nc : t) * kChunk, e = std::min(m, b + kChunk);
       if (is_off) {
         if (nonuniform.load(std::memory_order_relaxed)) continue;
         uint64_t bad = 0;
         for (uint64_t i = b; i < e; ++i) bad |= (off[i + 1] - off[i]) ^ d0;
         if (bad) nonuniform.store(true, std::memory_order_relaxed);
       } else {
-        if (nopack.load(std::memory_order_relaxed)) continue;
-        bool bad = false;
-        for (uint64_t i = b; i < e; ++i) {
-          const double x = w[i];
-          const uint32_t q = (x >= 1.0 && x <= 255.0) ? static_cast<uint32_t>(x) : 0u;
-          bad |= static_cast<double>(q) != x;
-          packed[i] = static_cast<uint8_t>(q);
+        if (!nopack.load(std::memory_order_relaxed)) {
+          bool bad = false;
+          for (uint64_t i = b; i < e; ++i) {
+            const double x = w[i];
+            const uint32_t q = (x >= 1.0 && x <= 255.0) ? static_cast<uint32_t>(x) : 0u;
+            bad |= static_cast<double>(q) != x;
+            packed[i] = static_cast<uint8_t>(q);
+          }
+          if (bad) nopack.store(true, std::memory_order_relaxed);
         }
-        if (bad) nopack.store(true, std::memory_order_relaxed);
+        weight_chunks_done.fetch_add(1, std::memory_order_release);
       }
     }
   }
+  bool weights_ready() const { return weight_chunks_done.load(std::memory_order_acquire) == chunks_per_array(); }
 };
 
 static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const UploadPlan& plan = UploadPlan()) {
@@ -467,8 +490,10 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   }
   cudaStream_t s = g->stream;
   int rc;
+  PhaseTrace tr;
   if ((rc = dev_alloc(&g->pins, g->kappa, g)) != HLM_B200_OK) return fail(rc);
   if ((rc = dev_alloc(&g->base, m, g)) != HLM_B200_OK) return fail(rc);
+  tr.mark("upload: device alloc");
 
   // ---- host-assisted path: scan / pack on the host cores while the pins cross PCIe
   const unsigned hc = std::thread::hardware_concurrency();
@@ -486,47 +511,48 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     if (!scan.packed) scan.nopack = true;
     if (scan.d0 == 0 || scan.d0 > kLargeEdge) scan.nonuniform = true;  // plain path handles these
     const unsigned nt = std::min(hc, 32u);
-    for (unsigned t = 0; t + 1 < nt; ++t) workers.emplace_back([&scan] { scan.work(); });
+    for (unsigned t = 0; t + 1 < nt; ++t) workers.emplace_back([&scan] { scan.work([] {}); });
   }
   cudaError_t e = cudaSuccess;
   if (g->kappa) e = cudaMemcpyAsync(g->pins, h->edge_members, g->kappa * 4, cudaMemcpyHostToDevice, s);
   g->h2d_bytes = g->kappa * 4;
-  if (assist) {
-    scan.work();  // this thread helps once the copy is queued
-    for (auto& t : workers) t.join();
-  }
-  auto drop_packed = [&]() {
-    if (scan.packed) host_result_free(scan.packed);
-    scan.packed = nullptr;
-  };
-  if (e != cudaSuccess) {
-    drop_packed();
-    set_error("host-to-device copy failed: %s", cudaGetErrorString(e));
-    return fail(HLM_B200_ERR_CUDA);
-  }
-  const bool uniform_known = assist && !scan.nonuniform.load();
-  const bool packed_ok = assist && !scan.nopack.load();
+  tr.mark("upload: pins copy queued");
 
-  // ---- weights
-  if (m) {
-    if (packed_ok) {
-      uint8_t* d_codes = nullptr;
-      if ((rc = dev_alloc(&d_codes, m, nullptr)) != HLM_B200_OK) return drop_packed(), fail(rc);
+  // ---- weights: queued behind the pins as soon as the host has looked at all of them
+  uint8_t* d_codes = nullptr;
+  bool weights_queued = false;
+  auto queue_weights = [&]() {
+    if (weights_queued || !m || e != cudaSuccess || rc != HLM_B200_OK) return;
+    if (assist && !scan.weights_ready()) return;
+    weights_queued = true;
+    if (assist && !scan.nopack.load()) {
+      if ((rc = dev_alloc(&d_codes, m, nullptr)) != HLM_B200_OK) return;
       e = cudaMemcpyAsync(d_codes, scan.packed, m, cudaMemcpyHostToDevice, s);
       k_expand_u8<<<grid_for(g, m), kBlock, 0, s>>>(d_codes, m, g->base);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-      pool_free(d_codes);
       g->h2d_bytes += m;
     } else {
       e = cudaMemcpyAsync(g->base, h->base_weights, static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, s);
       g->h2d_bytes += static_cast<uint64_t>(m) * 8;
     }
+  };
+  rc = HLM_B200_OK;
+  if (assist) {
+    scan.work(queue_weights);  // this thread helps once the copy is queued
+    for (auto& t : workers) t.join();
   }
-  drop_packed();
+  queue_weights();
+  tr.mark("upload: host scan + pack");
+  if (e == cudaSuccess && rc == HLM_B200_OK) e = cudaStreamSynchronize(s);
+  pool_free(d_codes);
+  if (scan.packed) host_result_free(scan.packed);
+  scan.packed = nullptr;
+  if (rc != HLM_B200_OK) return fail(rc);
   if (e != cudaSuccess) {
     set_error("host-to-device copy failed: %s", cudaGetErrorString(e));
     return fail(HLM_B200_ERR_CUDA);
   }
+  const bool uniform_known = assist && !scan.nonuniform.load();
+  tr.mark("upload: copies done");
 
   // ---- edge structure
   if (uniform_known) {
@@ -566,8 +592,11 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     g->h2d_bytes += (static_cast<uint64_t>(m) + 1) * 8;
     if ((rc = finish_graph(g, off64, true)) != HLM_B200_OK) return fail(rc);
   }
+  tr.mark("upload: edge structure");
   if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
+  tr.mark("upload: weight stats");
   if (plan.reorder && reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
+  if (plan.reorder) tr.mark("upload: first-pin sort");
   *out = g;
   return HLM_B200_OK;
 }
@@ -955,8 +984,10 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     return HLM_B200_ERR_UNSUPPORTED;
   }
   cudaStream_t s = g->stream;
+  PhaseTrace tr;
   ST_CHECK(ensure_workspace(g, max_rounds));
   Workspace& w = g->ws;
+  tr.mark("match: workspace");
 
   Launcher L;
   ST_CHECK(setup_launcher(g, st, cfg, max_rounds, L, nullptr, false));
@@ -968,6 +999,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     ST_CHECK(build_loop_graph(L, 0));
   }
 
+  tr.mark("match: launcher + graph");
   CU_CHECK(cudaEventRecord(w.ev0, s));
   // per-call state
   Ctrl c0;
@@ -1081,7 +1113,9 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
       out->round_check_ms[i] = t_check[i];
     }
   }
+  tr.mark("match: rounds");
   int rc = assemble_result(g, rounds, cfg, cfg->variant, out);
+  tr.mark("match: result");
   if (rc != HLM_B200_OK) return rc;
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
@@ -1397,11 +1431,15 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   Graph* g = nullptr;
   UploadPlan plan;
   plan.reorder = false;  // a single matching does not repay the 40 ms first-pin sort (9.2 vs 7.9 ms)
+  PhaseTrace tr;
   int rc = upload(host, device, &g, plan);
   if (rc != HLM_B200_OK) return rc;
+  tr.mark("match_host: upload");
   rc = run_match(g, stream, cfg, out);
+  tr.mark("match_host: match");
   out->h2d_bytes = g->h2d_bytes;
   delete g;
+  tr.mark("match_host: release");
   return rc;
 }
 
