@@ -248,16 +248,25 @@ def main():
         raise SystemExit("bench.py needs a CUDA device: the matching path has no CPU fallback")
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    # HLM_BENCH_FORCE_MG=1 runs the edge-partitioned (multi-GPU) driver even with one rank: the only
+    # way to exercise that code path on a single-GPU box
+    sharded = world > 1 or os.environ.get("HLM_BENCH_FORCE_MG") == "1"
+    if sharded:
         import torch.distributed as dist_mod
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist = dist_mod
-    if world > 1:
         from paper_2602_22976_b200 import multi_gpu
 
-        multi_gpu.bench_main(args, wl, rank, world, local_rank, dist)
+        hbm_gbs, peak_src = load_peaks()
+        multi_gpu.bench_main(args, wl, rank, world, local_rank, dist,
+                             extras=dict(sampler=ClockSampler(local_rank) if rank == 0 else None,
+                                         algorithmic_bytes=algorithmic_bytes, hbm_gbs=hbm_gbs, peak_src=peak_src))
+        dist_mod.destroy_process_group()
         return
 
     hbm_gbs, peak_src = load_peaks()

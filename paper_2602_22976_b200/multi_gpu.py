@@ -379,7 +379,7 @@ def virtual_cluster(family: str, world: int, device: int = 0, **spec) -> Sharded
     return ShardedMatcher(engines, m, kappa, Collectives())
 
 
-def bench_main(args, wl, rank, world, local_rank, dist):
+def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
     """bench.py --gpus N (N > 1): config 5 shape, weak scaling -- every rank owns 250 M edges of an
     8-uniform instance with n = 125 M * N vertices (N = 8 is BASELINE config 5 exactly)."""
     import torch
@@ -394,8 +394,12 @@ def bench_main(args, wl, rank, world, local_rank, dist):
     sm = ShardedMatcher([eng], m, m * d, coll)
     stream = WeightStream()
     cfg = ParallelConfig(variant="crcw")
-    for _ in range(max(1, min(args.warmup, 3))):
+    extras = extras or {}
+    for _ in range(max(3, args.warmup)):
         res = sm.match(stream, cfg, gather=False)
+    sampler = extras.get("sampler")
+    if sampler:
+        sampler.start()
     dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -408,10 +412,24 @@ def bench_main(args, wl, rank, world, local_rank, dist):
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
+    clocks = sampler.stop() if sampler else None
     if rank == 0:
         value = m * d * args.steps / (total_ms * 1e-3)
+        roofline = None
+        if extras.get("algorithmic_bytes"):
+            # whole job, all ranks: algorithmic bytes of the rounds over the step time,
+            # against N x the measured HBM peak (collective time is inside the step)
+            total_bytes, _, _ = extras["algorithmic_bytes"](m * d, m, n, d, res.report.matched_per_round_count,
+                                                            res.report.deactivated_per_round)
+            achieved = total_bytes / (total_ms / args.steps * 1e-3) / 1e9
+            peak = extras["hbm_gbs"] * world
+            roofline = {"bound": "hbm", "kernel": "whole job (round sweeps + checks + collectives), all ranks",
+                        "achieved": achieved, "peak": peak, "peak_source": extras["peak_src"] + f" x {world} GPUs",
+                        "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                        "collective_ms_per_step": sm.timings.get("collective_ms"),
+                        "collective_bytes_per_step": sm.timings.get("collective_bytes")}
         line = {"metric": "pins_per_sec_to_maximal_matching", "value": value, "unit": "pins/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "u64 keys (f64 weights, u32 ids)", "data": "synthetic",
                 "config": {"workload": f"config 5 shape: 8-uniform, n={n}, m={m} edge-partitioned over {world} GPUs "
@@ -421,6 +439,10 @@ def bench_main(args, wl, rank, world, local_rank, dist):
                            "collective_ms_last_step": sm.timings.get("collective_ms"),
                            "l2_policy": "inputs larger than L2; no flush"},
                 "gpu_launches": int(res.report.kernel_launches) * args.steps,
+                "clocks": clocks, "roofline": roofline,
+                "cpu_baseline": {"value": None, "unit": "pins/s", "cores": 0, "kind": "unavailable",
+                                 "sample": "N > 1: the CPU baseline is reported by the N = 1 run (config 5 does not "
+                                           "fit host memory)"},
                 "e2e": {"value": value, "unit": "pins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "note": "instance generated on the devices (16 G pins do not fit host memory)"}}
         print(json.dumps(line), flush=True)
