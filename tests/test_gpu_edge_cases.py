@@ -164,3 +164,23 @@ def test_many_rounds_epoch_wrap(hb, port):
             assert got.report.graph_launches >= 3  # one relaunch per tag epoch
     assert_same_result(hb.run_variant(to_hb_graph(g), to_hb_stream(z), hb.ParallelConfig(variant="crew", max_rounds=400)),
                        want, "long chain crew")
+
+
+@pytest.mark.parametrize("d", [2, 4, 8])
+@pytest.mark.parametrize("resident", [False, True])
+def test_ties_on_the_uniform_kernels(hb, port, d, resident):
+    """Equal 64-bit keys on the uniform-size sweeps (round-1 pipelined kernel with the deferred tie
+    check, later-round kernels, d = 8 without deferral), both for the caller's edge order (one-shot
+    call) and for the first-pin sorted resident instance: detected, redone exactly, same result."""
+    g = port.syn_generate(po.SYN_UNIFORM, n=600, m=6000, d=d, seed=11 + d)
+    s = po.Stream(seed=5, kind=po.GEN_PARK_MILLER, noise_low=0.0, noise_high=2.0 ** -50)
+    want = port.local_max(g, s)
+    for loop in ("graph", "host"):
+        cfg = hb.ParallelConfig(variant="crcw", loop_mode=loop)
+        if resident:
+            with hb.DeviceHypergraph.upload(to_hb_graph(g)) as dg:
+                got = dg.match(to_hb_stream(s), cfg)
+        else:
+            got = hb.run_variant(to_hb_graph(g), to_hb_stream(s), cfg)
+        assert_same_result(got, want, f"uniform d={d} resident={resident} {loop}")
+        assert got.report.tie_redo_rounds >= 1
