@@ -62,6 +62,11 @@ bool reorder_enabled() {
   return !(env && env[0] == '0');
 }
 
+bool renumber_enabled() {
+  const char* env = std::getenv("HLM_B200_RENUMBER");
+  return !(env && env[0] == '0');
+}
+
 uint32_t default_max_rounds(uint32_t m) {  // matching.hpp:87-89, common.hpp:27-35
   const uint64_t x = static_cast<uint64_t>(m) + 2;
   uint32_t r = 0;
@@ -241,6 +246,7 @@ Graph::~Graph() {
   dev_free(base);
   dev_free(large_list);
   dev_free(orig);
+  dev_free(vold);
   dev_free(base_run);
   dev_free(voff);
   dev_free(vinc);
@@ -595,6 +601,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   tr.mark("upload: edge structure");
   if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
   tr.mark("upload: weight stats");
+  if (plan.reorder && reorder_enabled() && renumber_enabled() && (rc = renumber_by_degree(g)) != HLM_B200_OK) return fail(rc);
   if (plan.reorder && reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
   if (plan.reorder) tr.mark("upload: first-pin sort");
   *out = g;
@@ -928,6 +935,12 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   // survivors read vtop.  Measured: config 3 45.7 -> 38.2 ms, 8-uniform 167 -> 141 ms, config 2
   // 7.8 -> 7.6 ms; 0 restores the single gather per pin.
   P.dead_first = 1u;
+  // hot windows (ids below these are loaded with ld.ca, the rest bypass L1)
+  // without renumbering every id may be hot (hubs sit anywhere): everything through L1, as before
+  P.hot_vtop = g->vold ? 32768u : 0xFFFFFFFFu;     // 128 KB of filter words
+  P.hot_bits = g->vold ? (1u << 20) : 0xFFFFFFFFu;  // 128 KB of dead bits
+  if (const char* env = std::getenv("HLM_B200_HOT_VTOP")) P.hot_vtop = static_cast<uint32_t>(std::strtoul(env, nullptr, 10));
+  if (const char* env = std::getenv("HLM_B200_HOT_BITS")) P.hot_bits = static_cast<uint32_t>(std::strtoul(env, nullptr, 10));
   if (const char* env = std::getenv("HLM_B200_DEAD_FIRST")) P.dead_first = env[0] == '1';
   P.mbits = w.mbits;
   P.mround = w.mround;
@@ -1428,6 +1441,10 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
                         const hlm_b200_config* cfg, int device, hlm_b200_result* out) {
   if (!out) return HLM_B200_ERR_INPUT;
   std::memset(out, 0, sizeof(*out));
+  if (!stream || !cfg) {
+    set_error("null argument");
+    return HLM_B200_ERR_INPUT;
+  }
   Graph* g = nullptr;
   UploadPlan plan;
   plan.reorder = false;  // a single matching does not repay the 40 ms first-pin sort (9.2 vs 7.9 ms)
@@ -1435,6 +1452,11 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   int rc = upload(host, device, &g, plan);
   if (rc != HLM_B200_OK) return rc;
   tr.mark("match_host: upload");
+  // a single matching: building the CUDA graph (0.3 ms) costs more than the host loop's per-round
+  // synchronisations save
+  hlm_b200_config one_shot = *cfg;
+  if (one_shot.loop_mode == HLM_B200_LOOP_AUTO) one_shot.loop_mode = HLM_B200_LOOP_HOST;
+  cfg = &one_shot;
   rc = run_match(g, stream, cfg, out);
   tr.mark("match_host: match");
   out->h2d_bytes = g->h2d_bytes;

@@ -78,6 +78,7 @@ struct Graph {
   uint32_t num_large = 0;
   uint32_t* large_list = nullptr;
   double* base = nullptr;  // null: all weights equal base_const (caller's edge order)
+  uint32_t* vold = nullptr;     // resident vertex v is the caller's vertex vold[v] (null: same numbering)
   uint32_t* orig = nullptr;     // resident edge e is the caller's edge orig[e] (null: same order)
   double* base_run = nullptr;   // base weights in resident order when orig != null
   double base_const = 1.0;
@@ -113,8 +114,10 @@ int weight_stats(Graph* g, double lo, WeightStats* out);
 int build_incidence(Graph* g);
 int ensure_workspace(Graph* g, uint32_t max_rounds);
 bool reorder_enabled();
+bool renumber_enabled();
 int reorder_by_first_pin(Graph* g);
-int download_pins_original_order(Graph* g, uint32_t* host_pins);
+int renumber_by_degree(Graph* g);
+int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins);
 int generate(const hlm_b200_syn_spec* spec, int device, Graph** out);
 int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base);
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);

@@ -10,9 +10,6 @@ namespace hlmb {
 // Round kernels, class 0: one thread per edge (size <= kLargeEdge), ITEMS edges per thread and
 // tile.  D > 0: uniform edge size, one 64/128-bit pin load per edge; D == 0: runtime offsets.
 // ---------------------------------------------------------------------------------------------
-#ifndef HLM_VTOP_LD
-#define HLM_VTOP_LD __ldca  // L1 may serve hub vertices: stale values are only ever too small (safe)
-#endif
 #ifndef HLM_SWEEP_MIN_BLOCKS
 #define HLM_SWEEP_MIN_BLOCKS 4  // 64 registers: four batches of a warp are in flight at once
 #endif
@@ -130,10 +127,10 @@ struct SweepCtx {
     if (peek && b.live) {
       if (dead_first) {
 #pragma unroll
-        for (int i = 0; i < D; ++i) b.cur[i] = dead_word(P.dead_all, b.pv.v[i]);
+        for (int i = 0; i < D; ++i) b.cur[i] = (is_dead(P, b.pv.v[i]) ? kTopDead : 0u);
       } else {
 #pragma unroll
-        for (int i = 0; i < D; ++i) b.cur[i] = HLM_VTOP_LD(P.vtop + b.pv.v[i]);
+        for (int i = 0; i < D; ++i) b.cur[i] = ld_top(P, b.pv.v[i]);
       }
     }
     // ---- stage A: ids and pins of batch it
@@ -170,7 +167,7 @@ struct SweepCtx {
         c1.base = base_of(P, c1.e);
         if (dead_first) {  // only the survivors pay for the (HBM-resident) filter words
 #pragma unroll
-          for (int i = 0; i < D; ++i) c1.cur[i] = HLM_VTOP_LD(P.vtop + c1.pv.v[i]);
+          for (int i = 0; i < D; ++i) c1.cur[i] = ld_top(P, c1.pv.v[i]);
         }
       }
     }
@@ -327,17 +324,17 @@ __global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundP
           bool dead_any = false;
           if (dead_first) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) dead_any |= vertex_dead(P.dead_all, pv.v[i]);
+            for (int i = 0; i < D; ++i) dead_any |= is_dead(P, pv.v[i]);
             if (VMAX && !dead_any) {
 #pragma unroll
-              for (int i = 0; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+              for (int i = 0; i < D; ++i) cur[i] = ld_top(P, pv.v[i]);
             }
           } else {
-            cur[0] = HLM_VTOP_LD(P.vtop + pv.v[0]);
+            cur[0] = ld_top(P, pv.v[0]);
             dead_any = cur[0] == kTopDead;
             if (!dead_any) {
 #pragma unroll
-              for (int i = 1; i < D; ++i) cur[i] = HLM_VTOP_LD(P.vtop + pv.v[i]);
+              for (int i = 1; i < D; ++i) cur[i] = ld_top(P, pv.v[i]);
 #pragma unroll
               for (int i = 1; i < D; ++i) dead_any |= (cur[i] == kTopDead);
             }
@@ -447,11 +444,11 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
             bool dead_any = false;
             if (dead_first) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && vertex_dead(P.dead_all, v[i]));
+              for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && is_dead(P, v[i]));
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              cur[i] = (peek && !dead_any && static_cast<uint32_t>(i) < s) ? HLM_VTOP_LD(P.vtop + v[i]) : 0u;
+              cur[i] = (peek && !dead_any && static_cast<uint32_t>(i) < s) ? ld_top(P, v[i]) : 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
             if (dead_any) {
@@ -489,8 +486,8 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
         const bool mine = lane < es;
         const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
         const bool peek = r > 1 || P.ks.precheck;
-        bool dead_any = dead_first && __any_sync(0xffffffffu, mine && vertex_dead(P.dead_all, v));
-        const uint32_t cur = (mine && peek && !dead_any) ? HLM_VTOP_LD(P.vtop + v) : 0u;
+        bool dead_any = dead_first && __any_sync(0xffffffffu, mine && is_dead(P, v));
+        const uint32_t cur = (mine && peek && !dead_any) ? ld_top(P, v) : 0u;
         dead_any = dead_any || __any_sync(0xffffffffu, mine && cur == kTopDead);
         bool lost = false;
         if (!dead_any) {
@@ -716,7 +713,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
         bool d = false;
         if (i < s) {
           const uint32_t v = __ldg(pp + i);
-          d = use_bits ? vertex_dead(P.dead_all, v) : (__ldcg(P.vtop + v) == kTopDead);
+          d = use_bits ? is_dead(P, v) : (__ldcg(P.vtop + v) == kTopDead);
         }
         dead_any = __any_sync(0xffffffffu, d);
       }

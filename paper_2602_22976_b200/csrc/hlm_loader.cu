@@ -174,29 +174,35 @@ __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, const unsigned l
   }
 }
 
-int build_incidence(Graph* g) {
-  if (g->voff) return HLM_B200_OK;
+// voff (n+1) / vinc (kappa) of the CSR `csr` over n vertices; edges are named by orig[] when given
+static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc) {
   cudaStream_t s = g->stream;
   uint32_t* deg = nullptr;
   ST_CHECK(dalloc(&deg, g->n));
-  ST_CHECK(dalloc(&g->voff, static_cast<size_t>(g->n) + 1));
-  ST_CHECK(dalloc(&g->vinc, g->kappa));
-  g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
   CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
-  if (g->kappa) k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, deg);
-  int rc = device_exclusive_scan_u32_to_u64(g, deg, g->voff, g->n, nullptr);
+  if (g->kappa) k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(csr.pins, g->kappa, deg);
+  int rc = device_exclusive_scan_u32_to_u64(g, deg, voff, g->n, nullptr);
   if (rc != HLM_B200_OK) {
     pool_free(deg);
     return rc;
   }
   CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
   if (g->m)
-    k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(
-        g->csr(), g->m, reinterpret_cast<const unsigned long long*>(g->voff), deg, g->orig, g->vinc);
+    k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(csr, g->m, reinterpret_cast<const unsigned long long*>(voff),
+                                                         deg, g->orig, vinc);
   CU_CHECK(cudaStreamSynchronize(s));
   pool_free(deg);
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
+}
+
+// the resident instance's own incidence side (resident vertex numbering), kept for the CREW variant
+int build_incidence(Graph* g) {
+  if (g->voff) return HLM_B200_OK;
+  ST_CHECK(dalloc(&g->voff, static_cast<size_t>(g->n) + 1));
+  ST_CHECK(dalloc(&g->vinc, g->kappa));
+  g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
+  return build_incidence_into(g, g->csr(), g->voff, g->vinc);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -403,6 +409,9 @@ int generate(const hlm_b200_syn_spec* spec, int device, Graph** out) {
     set_error("synthetic generation failed: %s", cudaGetErrorString(e));
     return fail(HLM_B200_ERR_CUDA);
   }
+  if (reorder_enabled() && renumber_enabled() && begin == 0 && m_local == spec->m &&
+      (rc = renumber_by_degree(g)) != HLM_B200_OK)
+    return fail(rc);
   if (reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
   *out = g;
   return HLM_B200_OK;
@@ -423,6 +432,12 @@ __global__ void k_widen_offsets(const EdgeCsr csr, uint32_t m, unsigned long lon
   }
 }
 
+__global__ void k_map_pins(const uint32_t* pins, uint64_t kappa, const uint32_t* map, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < kappa;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = __ldg(map + pins[i]);
+}
+
 __global__ void k_fill_const(double* out, uint32_t m, double v) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) out[e] = v;
 }
@@ -438,7 +453,16 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
     CU_CHECK(cudaStreamSynchronize(s));
     pool_free(tmp);
   }
-  if (pins && g->kappa) ST_CHECK(download_pins_original_order(g, pins));
+  // the caller's vertex numbering: pins of the resident rows mapped back through vold[]
+  uint32_t* old_pins = nullptr;  // resident edge order, caller's vertex ids
+  if (g->vold && g->kappa && (pins || voff || vinc)) {
+    ST_CHECK(dalloc(&old_pins, g->kappa));
+    k_map_pins<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, g->vold, old_pins);
+  }
+  if (pins && g->kappa) {
+    const int rc = download_pins_original_order(g, old_pins ? old_pins : g->pins, pins);
+    if (rc != HLM_B200_OK) return pool_free(old_pins), rc;
+  }
   if (base && g->m) {
     if (g->base) {
       CU_CHECK(cudaMemcpyAsync(base, g->base, static_cast<size_t>(g->m) * 8, cudaMemcpyDeviceToHost, s));
@@ -452,13 +476,34 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
     }
   }
   if (voff || vinc) {
-    ST_CHECK(build_incidence(g));
-    if (voff)
-      CU_CHECK(cudaMemcpyAsync(voff, g->voff, (static_cast<size_t>(g->n) + 1) * 8, cudaMemcpyDeviceToHost, s));
-    if (vinc && g->kappa)
-      CU_CHECK(cudaMemcpyAsync(vinc, g->vinc, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+    const uint64_t* d_voff = nullptr;
+    const uint32_t* d_vinc = nullptr;
+    uint64_t* t_voff = nullptr;
+    uint32_t* t_vinc = nullptr;
+    if (old_pins) {  // renumbered instance: the incidence side in the caller's numbering is built on the fly
+      int rc = dalloc(&t_voff, static_cast<size_t>(g->n) + 1);
+      if (rc == HLM_B200_OK) rc = dalloc(&t_vinc, g->kappa);
+      if (rc == HLM_B200_OK) {
+        EdgeCsr csr = g->csr();
+        csr.pins = old_pins;
+        rc = build_incidence_into(g, csr, t_voff, t_vinc);
+      }
+      if (rc != HLM_B200_OK) return pool_free(old_pins), pool_free(t_voff), pool_free(t_vinc), rc;
+      d_voff = t_voff;
+      d_vinc = t_vinc;
+    } else {
+      ST_CHECK(build_incidence(g));
+      d_voff = g->voff;
+      d_vinc = g->vinc;
+    }
+    if (voff) CU_CHECK(cudaMemcpyAsync(voff, d_voff, (static_cast<size_t>(g->n) + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (vinc && g->kappa) CU_CHECK(cudaMemcpyAsync(vinc, d_vinc, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+    pool_free(t_voff);
+    pool_free(t_vinc);
   }
   CU_CHECK(cudaStreamSynchronize(s));
+  pool_free(old_pins);
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
 }
@@ -556,19 +601,102 @@ int reorder_by_first_pin(Graph* g) {
   return HLM_B200_OK;
 }
 
-int download_pins_original_order(Graph* g, uint32_t* host_pins) {
+int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins) {
   cudaStream_t s = g->stream;
   if (!g->orig) {
-    CU_CHECK2(cudaMemcpyAsync(host_pins, g->pins, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+    CU_CHECK2(cudaMemcpyAsync(host_pins, resident_pins, g->kappa * 4, cudaMemcpyDeviceToHost, s));
+    CU_CHECK2(cudaStreamSynchronize(s));
     return HLM_B200_OK;
   }
   uint32_t* tmp = nullptr;
   ST_CHECK(dalloc(&tmp, g->kappa));
-  k_unpermute_rows<<<grid_of(g, g->m), kBlock, 0, s>>>(g->pins, g->orig, g->m, g->uniform_d, tmp);
+  k_unpermute_rows<<<grid_of(g, g->m), kBlock, 0, s>>>(resident_pins, g->orig, g->m, g->uniform_d, tmp);
   CU_CHECK2(cudaMemcpyAsync(host_pins, tmp, g->kappa * 4, cudaMemcpyDeviceToHost, s));
   CU_CHECK2(cudaStreamSynchronize(s));
   pool_free(tmp);
   return HLM_B200_OK;
+}
+
+}  // namespace hlmb
+
+// ---------------------------------------------------------------------------------------------
+// Loader pass: renumber the vertices by descending degree (counting sort on the capped degree).
+// Vertex numbering is free (results name edges only).  With this order a vertex's id
+// says how hot it is: the filter words and dead bits of the most frequently touched vertices are
+// the first few hundred KB of their arrays and stay resident in the SM's L1 (loads of hot ids use
+// ld.ca, cold ids bypass L1 with ld.cg so they cannot evict the hot window).  An L1 hit costs a
+// third of an L2 sector request (scripts/micro/gather_bench.cu: 860 vs 285 G gathers/s), and the
+// round sweeps are bound by exactly that rate.
+// ---------------------------------------------------------------------------------------------
+namespace hlmb {
+
+constexpr uint32_t kDegCap = 65535;
+
+__global__ void k_degree_hist(const uint32_t* deg, uint32_t n, uint32_t* hist) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t b = kDegCap - min(deg[v], kDegCap);  // bucket 0 = the highest degrees
+    // warp-aggregated: low-degree buckets receive millions of increments
+    const uint32_t peers = __match_any_sync(__activemask(), b);
+    if ((__ffs(peers) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(hist + b, __popc(peers));
+  }
+}
+
+__global__ void k_degree_rank(const uint32_t* deg, uint32_t n, const unsigned long long* start, uint32_t* cursor,
+                              uint32_t* new_id, uint32_t* old_id) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t b = kDegCap - min(deg[v], kDegCap);
+    const uint32_t peers = __match_any_sync(__activemask(), b);
+    const uint32_t lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (leader == static_cast<int>(lane)) base = atomicAdd(cursor + b, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const uint32_t id = static_cast<uint32_t>(start[b]) + base + __popc(peers & ((1u << lane) - 1u));
+    new_id[v] = id;
+    old_id[id] = v;
+  }
+}
+
+__global__ void k_remap_pins(uint32_t* pins, uint64_t kappa, const uint32_t* new_id) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < kappa;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    pins[i] = __ldg(new_id + pins[i]);
+}
+
+int renumber_by_degree(Graph* g) {
+  if (g->vold || g->n < 2 || g->kappa == 0) return HLM_B200_OK;
+  cudaStream_t s = g->stream;
+  uint32_t *deg = nullptr, *hist = nullptr, *new_id = nullptr;
+  uint64_t* start = nullptr;
+  const uint32_t nb = kDegCap + 1;
+  int rc = HLM_B200_OK;
+  auto cleanup = [&]() {
+    pool_free(deg);
+    pool_free(hist);
+    pool_free(start);
+    pool_free(new_id);
+  };
+  if ((rc = dalloc(&deg, g->n)) != HLM_B200_OK) return cleanup(), rc;
+  if ((rc = dalloc(&hist, nb)) != HLM_B200_OK) return cleanup(), rc;
+  if ((rc = dalloc(&start, static_cast<size_t>(nb) + 1)) != HLM_B200_OK) return cleanup(), rc;
+  if ((rc = dalloc(&new_id, g->n)) != HLM_B200_OK) return cleanup(), rc;
+  if ((rc = dalloc(&g->vold, g->n)) != HLM_B200_OK) return cleanup(), rc;
+  g->device_bytes += static_cast<uint64_t>(g->n) * 4;
+  CU_CHECK2(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
+  CU_CHECK2(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb) * 4, s));
+  k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, deg);
+  k_degree_hist<<<grid_of(g, g->n), kBlock, 0, s>>>(deg, g->n, hist);
+  rc = device_exclusive_scan_u32_to_u64(g, hist, start, nb, nullptr);
+  if (rc == HLM_B200_OK) {
+    CU_CHECK2(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb) * 4, s));
+    k_degree_rank<<<grid_of(g, g->n), kBlock, 0, s>>>(deg, g->n, reinterpret_cast<const unsigned long long*>(start),
+                                                      hist, new_id, g->vold);
+    k_remap_pins<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, new_id);
+    CU_CHECK2(cudaStreamSynchronize(s));
+    CU_CHECK2(cudaGetLastError());
+  }
+  cleanup();
+  return rc;
 }
 
 }  // namespace hlmb

@@ -96,6 +96,8 @@ struct RoundParams {
   uint32_t* vtop;            // n: high word of vkey, or kTopDead; the L2-resident filter array
   uint32_t* dead;            // n bits: where completion marking sets its bits (multi-GPU: the exchange area)
   const uint32_t* dead_all;  // n bits: every vertex covered so far; stable during a sweep
+  uint32_t hot_vtop;         // vertex ids below this keep their filter word in L1 (ld.ca); others ld.cg
+  uint32_t hot_bits;         // same for the dead bitmap
   uint32_t dead_first;       // sweeps of rounds >= 2 test the bitmap (n/8 bytes, L2-resident) before
                              // they touch vtop
   uint32_t* mbits;           // m bits: edge matched
@@ -156,6 +158,19 @@ __device__ __forceinline__ void mark_matched(const RoundParams& P, uint32_t e, u
 __device__ __forceinline__ void mark_dead(const RoundParams& P, uint32_t v) {
   P.vtop[v] = kTopDead;
   atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+}
+
+// Gathers of the per-vertex arrays by the sweeps.  Ids below the hot limits (the highest degrees
+// after the loader's renumbering) go through L1 (ld.ca; a stale filter word is only ever too small,
+// and dead bits never change during a sweep); all other ids bypass it (ld.cg) so that the random
+// cold accesses cannot evict the hot window.  Without renumbering the limits are 0 / everything.
+__device__ __forceinline__ uint32_t ld_top(const RoundParams& P, uint32_t v) {
+  return v < P.hot_vtop ? __ldca(P.vtop + v) : __ldcg(P.vtop + v);
+}
+__device__ __forceinline__ bool is_dead(const RoundParams& P, uint32_t v) {
+  const uint32_t* w = P.dead_all + (v >> 5);
+  const uint32_t bits = v < P.hot_bits ? __ldca(w) : __ldcg(w);
+  return (bits >> (v & 31)) & 1u;
 }
 
 // vkey[v] = max(vkey[v], key), vtop[v] = max(vtop[v], high word), filtered by `cur` = an earlier
