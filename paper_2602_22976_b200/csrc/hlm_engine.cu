@@ -204,6 +204,7 @@ void Workspace::release() {
     dev_free(seg_cnt[b]);
   }
   dev_free(large_state);
+  dev_free(bat_pin0);
   dev_free(cand_ids);
   dev_free(cand_cnt);
   dev_free(matched_cnt);
@@ -635,6 +636,11 @@ int ensure_workspace(Graph* g, uint32_t max_rounds) {
     ST_CHECK(dev_alloc(&w.large_state, g->num_large, g));
     ST_CHECK(dev_alloc(&w.cand_ids, static_cast<size_t>(w.nseg) * w.seg_cap, g));
     ST_CHECK(dev_alloc(&w.cand_cnt, w.nseg, g));
+    if (g->orig && g->uniform_d && g->m) {  // sorted by first pin: batch -> interval of first pins
+      const uint32_t entries = static_cast<uint32_t>((static_cast<uint64_t>(w.nseg) * w.seg_cap >> 5) + 2);
+      ST_CHECK(dev_alloc(&w.bat_pin0, entries, g));
+      k_batch_first_pins<<<grid_for(g, entries), kBlock, 0, g->stream>>>(g->pins, g->m, g->uniform_d, entries, w.bat_pin0);
+    }
     w.num_chunks = (w.mbits_words + kAsmChunkWords - 1) / kAsmChunkWords;
     ST_CHECK(dev_alloc(&w.chunk_cnt, w.num_chunks, g));
     ST_CHECK(dev_alloc(&w.scan_total, 1, g));
@@ -952,6 +958,7 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   P.large_state = w.large_state;
   P.num_large = g->num_large;
   P.nseg = w.nseg;
+  P.bat_pin0 = std::getenv("HLM_B200_NO_BATCH_SKIP") ? nullptr : w.bat_pin0;
   P.seg_cap = w.seg_cap;
   P.cand_ids = w.cand_ids;
   P.cand_cnt = w.cand_cnt;

@@ -23,6 +23,7 @@ struct Workspace {
   uint32_t* seg_cnt[2] = {nullptr, nullptr};
   uint32_t nseg = 0, seg_cap = 0;
   uint8_t* large_state = nullptr;
+  uint32_t* bat_pin0 = nullptr;  // first pin per 32-edge batch, first-pin sorted uniform instances only
   uint32_t* cand_ids = nullptr;
   uint32_t* cand_cnt = nullptr;
   uint32_t* matched_cnt = nullptr;

@@ -107,6 +107,9 @@ struct RoundParams {
   uint32_t* seg_cnt[2];      // [buffer][nseg] ids in use per region
   uint32_t nseg;
   uint32_t seg_cap;
+  const uint32_t* bat_pin0;  // first pin of the first edge of every 32-edge batch, one entry more than
+                             // batches (first-pin sorted uniform instances; null otherwise): the first
+                             // pins of edges [32 a, 32 b) lie in [bat_pin0[a], bat_pin0[b]]
   uint32_t check_claim;      // regions a warp of the check kernel claims per ticket (1..8)
   uint32_t* cand_ids;        // class 0, same regions: edges that did not lose during vertex-max
   uint32_t* cand_cnt;        // [nseg]
