@@ -11,13 +11,16 @@ namespace hlmb {
 // tile.  D > 0: uniform edge size, one 64/128-bit pin load per edge; D == 0: runtime offsets.
 // ---------------------------------------------------------------------------------------------
 #ifndef HLM_SWEEP_MIN_BLOCKS
-#define HLM_SWEEP_MIN_BLOCKS 4  // 64 registers: four batches of a warp are in flight at once
+#define HLM_SWEEP_MIN_BLOCKS 5  // d = 2: 48 registers for the four in-flight batches of a warp
+#endif
+#ifndef HLM_SWEEP_MIN_BLOCKS_D4
+#define HLM_SWEEP_MIN_BLOCKS_D4 3
+#endif
+#ifndef HLM_SWEEP_MIN_BLOCKS_D8
+#define HLM_SWEEP_MIN_BLOCKS_D8 2
 #endif
 #ifndef HLM_MIN_BLOCKS
 #define HLM_MIN_BLOCKS 8
-#endif
-#ifndef HLM_SWEEP_PEND_D2
-#define HLM_SWEEP_PEND_D2 2  // pending-tie register sets for d = 2 (atomics looked at two steps later)
 #endif
 
 __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
@@ -72,8 +75,9 @@ __device__ __forceinline__ bool span_all_dead(const RoundParams& P, uint32_t fir
 //                   fetch caller id + base weight
 //   C2 (batch t)    key of the edge (weight refresh, :126-135), atomicMax at the pins where it can
 //                   still raise the maximum (vertex argmax, :137-159), candidate list for the
-//                   check kernel.  The returning atomics' results are only looked at (tie
-//                   detection) one or two steps later.
+//                   check kernel.  (Keeping the returning atomics' results in registers for a
+//                   later step was measured and dropped: the compiler copies them at once, and the
+//                   extra registers cost a CTA per SM.)
 // The four batches live in four statically named register sets (the loop is unrolled by four and
 // the roles rotate), so no value that is still in flight is ever moved or touched early.
 // R1: the kernel launched for round 1 (identity list in and out, no dead vertices yet).
@@ -88,42 +92,13 @@ struct SweepSlot {
   double base;
 };
 
-// results of the returning atomics of one C2 step, not yet looked at
-template <int D>
-struct PendingTie {
-  unsigned long long key;
-  unsigned long long old[D];
-  __device__ __forceinline__ void clear() {
-    key = 0ull;
-#pragma unroll
-    for (int i = 0; i < D; ++i) old[i] = 1ull;
-  }
-  __device__ __forceinline__ bool hit() const {
-    bool t = false;
-#pragma unroll
-    for (int i = 0; i < D; ++i) t |= (old[i] == key);
-    return t;
-  }
-};
-
-// `old` keeps its value unless the atomic is performed: the destination register of the atomic
-// is the pending slot itself, so nothing waits for the result here.
-__device__ __forceinline__ void atomic_max_u64_if(bool pred, unsigned long long* addr, unsigned long long val,
-                                                  unsigned long long& old) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.max.u64 %0, [%1], %3;\n\t}"
-      : "+l"(old)
-      : "l"(addr), "r"(static_cast<uint32_t>(pred)), "l"(val)
-      : "memory");
-}
-
 template <int D>
 struct SweepState {
   uint32_t out_off, cand_off, local_deact;
   bool tie;
 };
 
-template <int D, bool VMAX, bool R1, int NPEND>
+template <int D, bool VMAX, bool R1>
 struct SweepCtx {
   const RoundParams& P;
   uint32_t r, tag, lane, lt_mask;
@@ -134,7 +109,7 @@ struct SweepCtx {
 
   // one pipeline step: stage A on `a`, B on `b`, C1 on `c1`, C2 on `c2`
   __device__ __forceinline__ void step(uint32_t it, SweepSlot<D>& a, SweepSlot<D>& b, SweepSlot<D>& c1,
-                                       SweepSlot<D>& c2, PendingTie<D>& pend, SweepState<D>& st) const {
+                                       SweepSlot<D>& c2, SweepState<D>& st) const {
     // ---- stage B: filter words of batch it-1
 #pragma unroll
     for (int i = 0; i < D; ++i) b.cur[i] = 0u;
@@ -192,23 +167,10 @@ struct SweepCtx {
         const unsigned long long key = priority_key(P.stream, P.ks, c2.oid + P.id_base, r, c2.base, tag);
         const uint32_t hi = static_cast<uint32_t>(key >> 32);
         bool lost = false;
-        if constexpr (NPEND > 0) {
-          st.tie |= pend.hit();  // atomics issued NPEND steps ago
-          pend.key = key;
 #pragma unroll
-          for (int i = 0; i < D; ++i) {
-            pend.old[i] = ~key;
-            const bool dep = c2.cur[i] <= hi;
-            atomic_max_u64_if(dep, P.vkey + c2.pv.v[i], key, pend.old[i]);
-            if (dep) atomicMax(P.vtop + c2.pv.v[i], hi);
-            lost |= !dep;  // a larger key was already there: cannot win this round
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < D; ++i) {
-            st.tie |= deposit_key(P, c2.pv.v[i], key, c2.cur[i]);
-            lost |= c2.cur[i] > hi;
-          }
+        for (int i = 0; i < D; ++i) {
+          st.tie |= deposit_key(P, c2.pv.v[i], key, c2.cur[i]);
+          lost |= c2.cur[i] > hi;  // a larger key was already there: cannot win this round
         }
         cand = !lost;
       }
@@ -221,18 +183,16 @@ struct SweepCtx {
 };
 
 template <int D>
-struct SweepTuning {  // CTAs per SM (register budget) and pending-tie sets per edge size
-  static constexpr int kMinBlocks = D == 2 ? HLM_SWEEP_MIN_BLOCKS : (D == 4 ? 3 : 2);
-  static constexpr int kPend = D == 2 ? HLM_SWEEP_PEND_D2 : (D == 4 ? 1 : 0);
+struct SweepTuning {  // CTAs per SM = register budget of the four in-flight batches (48 / 80 / 128 registers)
+  static constexpr int kMinBlocks = D == 2 ? HLM_SWEEP_MIN_BLOCKS : (D == 4 ? HLM_SWEEP_MIN_BLOCKS_D4 : HLM_SWEEP_MIN_BLOCKS_D8);
 };
 
 template <int D, bool VMAX, bool R1>
 __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_uniform(const RoundParams P) {
   static_assert(!R1 || VMAX, "round 1 without keys has nothing to do");
-  constexpr int NPEND = SweepTuning<D>::kPend;
   Ctrl* c = P.ctrl;
   const uint32_t par = c->parity;
-  SweepCtx<D, VMAX, R1, NPEND> X{P};
+  SweepCtx<D, VMAX, R1> X{P};
   X.r = c->round;
   X.tag = round_tag(P.ks, X.r);
   X.lane = threadIdx.x & 31;
@@ -249,9 +209,6 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   SweepState<D> st;
   st.local_deact = 0;
   st.tie = false;
-  PendingTie<D> pend0, pend1;
-  pend0.clear();
-  pend1.clear();
 
   const uint32_t gran = R1 ? 1u : claim_granularity(P, c->active_prev);
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
@@ -277,10 +234,10 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
     s0.live = s1.live = s2.live = s3.live = false;
     if (X.cnt) {
       for (uint32_t it = 0; it < steps; it += 4u) {
-        X.step(it, s0, s3, s2, s1, pend0, st);
-        X.step(it + 1u, s1, s0, s3, s2, NPEND > 1 ? pend1 : pend0, st);
-        X.step(it + 2u, s2, s1, s0, s3, pend0, st);
-        X.step(it + 3u, s3, s2, s1, s0, NPEND > 1 ? pend1 : pend0, st);
+        X.step(it, s0, s3, s2, s1, st);
+        X.step(it + 1u, s1, s0, s3, s2, st);
+        X.step(it + 2u, s2, s1, s0, s3, st);
+        X.step(it + 3u, s3, s2, s1, s0, st);
       }
     }
     if (X.lane == 0) {
@@ -290,7 +247,6 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
       local_kept += kept;
     }
   }
-  if constexpr (NPEND > 0) st.tie |= pend0.hit() | pend1.hit();
   const uint32_t d = warp_sum(st.local_deact);
   if (X.lane == 0) {
     if (d) atomicAdd(P.deact_cnt + (X.r - 1), d);

@@ -12,6 +12,8 @@ elif which == "c3":
     dg = hb.DeviceHypergraph.generate("powerlaw", n=50_000_000, m=100_000_000, seed=1)
 elif which == "c4":
     dg = hb.DeviceHypergraph.generate("netlist", n=10_000_000, m=20_000_000, seed=1, int_weights=True)
+elif which == "u4":
+    dg = hb.DeviceHypergraph.generate("uniform", n=32_000_000, m=64_000_000, d=4, seed=1)
 elif which == "u8":
     dg = hb.DeviceHypergraph.generate("uniform", n=125_000_000, m=250_000_000, d=8, seed=1)
 best = None
