@@ -249,6 +249,7 @@ Graph::~Graph() {
   dev_free(orig);
   dev_free(vold);
   dev_free(base_run);
+  dev_free(base8);
   dev_free(voff);
   dev_free(vinc);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -367,6 +368,18 @@ int finish_weights(Graph* g) {
     g->device_bytes -= static_cast<size_t>(g->m) * 8;
     g->base = nullptr;
   }
+  return HLM_B200_OK;
+}
+
+// One byte per edge for the sweeps when every weight is an integer in 0..255 (resident order).
+int build_base_codes(Graph* g) {
+  if (g->base8 || !g->base || !g->base_integral || g->base_min < 0.0 || g->base_max > 255.0 || g->m == 0 ||
+      std::getenv("HLM_B200_NO_BASE8"))
+    return HLM_B200_OK;
+  ST_CHECK(dev_alloc(&g->base8, g->m, g));
+  const double* src = g->orig ? g->base_run : g->base;
+  k_pack_u8<<<grid_for(g, g->m), kBlock, 0, g->stream>>>(src, g->m, g->base8);
+  CU_CHECK(cudaStreamSynchronize(g->stream));
   return HLM_B200_OK;
 }
 
@@ -605,6 +618,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   if (plan.reorder && reorder_enabled() && renumber_enabled() && (rc = renumber_by_degree(g)) != HLM_B200_OK) return fail(rc);
   if (plan.reorder && reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
   if (plan.reorder) tr.mark("upload: first-pin sort");
+  if ((rc = build_base_codes(g)) != HLM_B200_OK) return fail(rc);
   *out = g;
   return HLM_B200_OK;
 }
@@ -760,7 +774,7 @@ struct Launcher {
     } else {
       // later rounds, d = 2, 4: the occupancy-driven sweep wins; d = 8: the pipelined one
       // (measured, profiles/README.md)
-      const int sgrid = g->num_sms * 8;
+      const int sgrid = g->num_sms * HLM_SIMPLE_MIN_BLOCKS;
       switch (g->uniform_d) {
         case 2: k_sweep_uniform_simple<2, VMAX><<<sgrid, kBlock, 0, s>>>(P); break;
         case 4: k_sweep_uniform_simple<4, VMAX><<<sgrid, kBlock, 0, s>>>(P); break;
@@ -910,6 +924,7 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   RoundParams& P = L.P;
   std::memset(&P, 0, sizeof(P));
   P.csr = g->csr();
+  P.base8 = g->base8;  // gathers of later rounds (base_of); round 1 streams the f64 array
   P.base = g->orig ? g->base_run : g->base;
   P.orig = g->orig;
   P.base_const = g->base_const;

@@ -82,6 +82,7 @@ struct Graph {
   uint32_t* vold = nullptr;     // resident vertex v is the caller's vertex vold[v] (null: same numbering)
   uint32_t* orig = nullptr;     // resident edge e is the caller's edge orig[e] (null: same order)
   double* base_run = nullptr;   // base weights in resident order when orig != null
+  uint8_t* base8 = nullptr;     // resident order, integer weights 0..255: what the gathers of rounds >= 2 read
   double base_const = 1.0;
   double base_min = 1.0, base_max = 1.0;
   bool base_integral = true;  // every base weight is an integer below 2^32 (order-free exact sums)
@@ -118,6 +119,7 @@ bool reorder_enabled();
 bool renumber_enabled();
 int reorder_by_first_pin(Graph* g);
 int renumber_by_degree(Graph* g);
+int build_base_codes(Graph* g);
 int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins);
 int generate(const hlm_b200_syn_spec* spec, int device, Graph** out);
 int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base);

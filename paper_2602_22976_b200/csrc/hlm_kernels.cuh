@@ -13,6 +13,9 @@ namespace hlmb {
 #ifndef HLM_SWEEP_MIN_BLOCKS
 #define HLM_SWEEP_MIN_BLOCKS 5  // d = 2: 48 registers for the four in-flight batches of a warp
 #endif
+#ifndef HLM_SIMPLE_MIN_BLOCKS
+#define HLM_SIMPLE_MIN_BLOCKS 8  // later-round sweep of d = 2, 4: 32 registers, 64 warps per SM
+#endif
 #ifndef HLM_SWEEP_MIN_BLOCKS_D4
 #define HLM_SWEEP_MIN_BLOCKS_D4 3
 #endif
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
 // Non-pipelined form of the same sweep: one batch per warp at a time, 32 registers, 64 resident
 // warps per SM.  Latency is hidden by occupancy instead of by the per-warp pipeline.
 template <int D, bool VMAX>
-__global__ void __launch_bounds__(kBlock, 8) k_sweep_uniform_simple(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform_simple(const RoundParams P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -960,6 +963,12 @@ __global__ void k_batch_first_pins(const uint32_t* pins, uint32_t m, uint32_t d,
     const uint64_t e = min(static_cast<uint64_t>(b) * 32u, static_cast<uint64_t>(m) - 1);
     bat_pin0[b] = pins[e * d];
   }
+}
+
+// loader: integer weights 0..255 in resident order, one byte each (see RoundParams::base8)
+__global__ void k_pack_u8(const double* __restrict__ base, uint32_t m, uint8_t* __restrict__ codes) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    codes[e] = static_cast<uint8_t>(base[e]);
 }
 
 // loader: weights the host packed to one byte each (integers 1..255) back to the resident f64 form

@@ -413,6 +413,7 @@ int generate(const hlm_b200_syn_spec* spec, int device, Graph** out) {
       (rc = renumber_by_degree(g)) != HLM_B200_OK)
     return fail(rc);
   if (reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);
+  if ((rc = build_base_codes(g)) != HLM_B200_OK) return fail(rc);
   *out = g;
   return HLM_B200_OK;
 }
