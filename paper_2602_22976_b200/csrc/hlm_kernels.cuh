@@ -36,10 +36,15 @@ __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool iden
 // One warp claims `gran` consecutive regions of the id space per ticket (no block barrier anywhere
 // in a sweep).  Same-address atomics retire at roughly one per nanosecond, so a kernel that takes
 // 75 K tickets cannot finish in less than ~60 us: sweeps over short lists claim 8 regions at a time.
-__device__ __forceinline__ uint32_t claim_region(uint32_t* ticket, uint32_t lane) {
+// Static-first mode (the check kernel): the first ticket of a warp is its own index in the grid, no
+// atomic, and the dynamic tickets follow behind the grid's warp count, so a short list costs the
+// warps that find nothing no atomic at all.  The sweeps do not use it: their first claims measured
+// slower that way on long lists, and the extra state spills in the 32-register kernel.
+__device__ __forceinline__ uint32_t grid_warp() { return blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); }
+__device__ __forceinline__ uint32_t claim_region(uint32_t* ticket, uint32_t lane, bool static_first) {
   uint32_t seg = 0;
   if (lane == 0) seg = atomicAdd(ticket, 1u);
-  return __shfl_sync(0xffffffffu, seg, 0);
+  return __shfl_sync(0xffffffffu, seg, 0) + (static_first ? gridDim.x * (blockDim.x >> 5) : 0u);
 }
 constexpr uint32_t kCoarseClaim = 8;
 __device__ __forceinline__ uint32_t claim_granularity(const RoundParams& P, uint32_t list_len) {
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   const uint32_t gran = R1 ? 1u : claim_granularity(P, c->active_prev);
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, X.lane) * gran;
+      seg = claim_region(&c->ticket_f, X.lane, false) * gran;
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform
   const uint32_t gran = claim_granularity(P, c->active_prev);
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, lane) * gran;
+      seg = claim_region(&c->ticket_f, lane, false) * gran;
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -399,7 +404,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
   const uint32_t gran = claim_granularity(P, c->active_prev);
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, lane) * gran;
+      seg = claim_region(&c->ticket_f, lane, false) * gran;
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -545,8 +550,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   const uint32_t lane = threadIdx.x & 31;
   uint32_t local_matched = 0, local_mpins = 0;
 
-  for (;;) {
-    const uint32_t seg0 = claim_region(&c->ticket_c, lane) * P.check_claim;
+  for (uint32_t ticket = grid_warp();; ticket = claim_region(&c->ticket_c, lane, true)) {
+    const uint32_t seg0 = ticket * P.check_claim;
     if (seg0 >= P.nseg) break;
     // end[j] = candidates in regions seg0 .. seg0+j (inclusive prefix), the same in every lane
     uint32_t mine = (lane < P.check_claim && seg0 + lane < P.nseg) ? list_cnt[seg0 + lane] : 0u;
