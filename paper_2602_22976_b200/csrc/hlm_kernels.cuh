@@ -23,7 +23,7 @@ namespace hlmb {
 #define HLM_SWEEP_MIN_BLOCKS_D8 2
 #endif
 #ifndef HLM_MIN_BLOCKS
-#define HLM_MIN_BLOCKS 8
+#define HLM_MIN_BLOCKS 6  // ragged-size sweep: 40 registers (8 CTAs/SM spill: config 3 38.2 -> 36.3 ms)
 #endif
 
 __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
