@@ -224,6 +224,35 @@ int hlm_b200_mg_end_round(hlm_b200_graph* g, uint32_t global_active, int* status
  * in ascending-id order, local_max_seq.hpp:79; FP64 addition is not associative). */
 int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result* out);
 
+/* ---- text formats (host only, no device needed) ------------------------------------------------
+ * io.hpp of the reference: hMetis .hgr hypergraphs (parse_hgr :79, write_hgr :146), METIS graphs
+ * as 2-uniform hypergraphs (parse_metis_graph :176), the matching file (write_matching :240,
+ * parse_matching :249), on top of build_hypergraph (hypergraph.hpp:78-153).  Same inputs accepted
+ * and rejected (HLM_B200_ERR_INPUT = hlm::input_error), same CSR and the same text out. */
+typedef struct {          /* an hlm::Hypergraph owned by the library: all five arrays, malloc'ed */
+  uint32_t num_vertices;
+  uint32_t num_edges;
+  uint64_t* vertex_offsets;
+  uint32_t* vertex_incidence;
+  uint64_t* edge_offsets;
+  uint32_t* edge_members;
+  double* base_weights;
+  uint32_t num_warnings;  /* ParseOptions::warnings->size(): 1 if a vertex-weight block was skipped */
+} hlm_b200_host_graph;
+
+/* hlm::DegreeZeroPolicy (hypergraph.hpp:56-59) */
+enum { HLM_B200_DEGREE_ZERO_REJECT = 0, HLM_B200_DEGREE_ZERO_DROP = 1 };
+
+int hlm_b200_parse_hgr(const char* text, size_t len, int degree_zero, hlm_b200_host_graph* out);
+int hlm_b200_parse_metis_graph(const char* text, size_t len, int degree_zero, hlm_b200_host_graph* out);
+void hlm_b200_host_graph_free(hlm_b200_host_graph* g);
+/* *text is NUL-terminated, *len excludes the NUL; release with hlm_b200_text_free */
+int hlm_b200_write_hgr(const hlm_b200_csr_view* h, char** text, size_t* len);
+int hlm_b200_write_matching(const uint32_t* matched, uint64_t count, double total_weight, uint32_t rounds,
+                            char** text, size_t* len);
+int hlm_b200_parse_matching(const char* text, size_t len, uint32_t** ids, uint64_t* count);
+void hlm_b200_text_free(void* p); /* texts and id arrays returned by the three calls above */
+
 /* default_max_rounds (matching.hpp:87-89). */
 uint32_t hlm_b200_default_max_rounds(uint32_t num_edges);
 

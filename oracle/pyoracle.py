@@ -288,6 +288,57 @@ class Oracle:
         self._fn("free_result", None, [C.c_void_p])(C.addressof(res))
         return out
 
+    # ---- reference only: io.hpp (text formats), for the parity tests of the library's parsers ----
+    def parse_text(self, which: str, text, degree_zero: int = 0):
+        """which: 'hgr' | 'metis'.  Returns (status, Graph or None, number of warnings)."""
+        assert self.kind == "reference"
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        og = COwnedGraph()
+        nw = C.c_uint32(0)
+        if which == "hgr":
+            f = self._fn("parse_hgr", C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p])
+            rc = f(data, len(data), degree_zero, C.addressof(og), C.addressof(nw))
+        else:
+            f = self._fn("parse_metis_graph", C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.c_void_p])
+            rc = f(data, len(data), degree_zero, C.addressof(og))
+        if rc != OK:
+            return rc, None, 0
+        g = _own_graph(og)
+        self._fn("free_graph", None, [C.c_void_p])(C.addressof(og))
+        return rc, g, int(nw.value)
+
+    def _text(self, ptr, length) -> str:
+        try:
+            return C.string_at(ptr, length.value).decode()
+        finally:
+            self._fn("free_text", None, [C.c_void_p])(ptr)
+
+    def write_hgr(self, g: Graph) -> str:
+        h = self.graph_handle(g)
+        try:
+            length = C.c_size_t()
+            ptr = self._fn("write_hgr", C.c_void_p, [C.c_void_p, C.c_void_p])(h, C.addressof(length))
+            return self._text(ptr, length)
+        finally:
+            self.graph_release(h)
+
+    def write_matching(self, matched, total_weight: float, rounds: int) -> str:
+        ids = np.ascontiguousarray(matched, dtype=np.uint32)
+        length = C.c_size_t()
+        f = self._fn("write_matching", C.c_void_p, [C.c_void_p, C.c_uint64, C.c_double, C.c_uint32, C.c_void_p])
+        return self._text(f(ids.ctypes.data if ids.size else None, ids.size, total_weight, rounds, C.addressof(length)), length)
+
+    def parse_matching(self, text):
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        ptr, cnt = C.POINTER(C.c_uint32)(), C.c_uint64()
+        f = self._fn("parse_matching", C.c_int, [C.c_char_p, C.c_size_t, C.c_void_p, C.c_void_p])
+        rc = f(data, len(data), C.addressof(ptr), C.addressof(cnt))
+        if rc != OK:
+            return rc, None
+        out = _take(ptr, cnt.value, np.uint32)
+        self._fn("free_text", None, [C.c_void_p])(C.cast(ptr, C.c_void_p))
+        return rc, out
+
     def hardware_workers(self) -> int:
         if self.kind == "reference":
             return int(self._fn("hardware_workers", C.c_uint, [])())

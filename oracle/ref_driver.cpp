@@ -183,6 +183,74 @@ int ref_tie_break(double wa, uint32_t ida, double wb, uint32_t idb, const orc_st
 
 uint32_t ref_default_max_rounds(uint32_t m) { return hlm::default_max_rounds(m); }
 
+// ---- io.hpp: the reference's own parsers and writers, for the text-format parity tests ----------
+static hlm::ParseOptions parse_options(int degree_zero, std::vector<std::string>* warnings) {
+  hlm::ParseOptions o;
+  o.degree_zero = degree_zero ? hlm::DegreeZeroPolicy::drop_and_renumber : hlm::DegreeZeroPolicy::reject;
+  o.warnings = warnings;
+  return o;
+}
+
+int ref_parse_hgr(const char* text, size_t len, int degree_zero, orc_owned_graph* out, uint32_t* num_warnings) {
+  std::memset(out, 0, sizeof(*out));
+  std::vector<std::string> warnings;
+  try {
+    export_graph(hlm::parse_hgr(std::string(text, len), parse_options(degree_zero, &warnings)), out);
+    if (num_warnings) *num_warnings = static_cast<uint32_t>(warnings.size());
+    return ORC_OK;
+  } catch (const hlm::input_error&) {
+    return ORC_INPUT_ERROR;
+  }
+}
+
+int ref_parse_metis_graph(const char* text, size_t len, int degree_zero, orc_owned_graph* out) {
+  std::memset(out, 0, sizeof(*out));
+  try {
+    export_graph(hlm::parse_metis_graph(std::string(text, len), parse_options(degree_zero, nullptr)), out);
+    return ORC_OK;
+  } catch (const hlm::input_error&) {
+    return ORC_INPUT_ERROR;
+  }
+}
+
+static char* dup_text(const std::string& s, size_t* len) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size());
+  p[s.size()] = 0;
+  *len = s.size();
+  return p;
+}
+
+char* ref_write_hgr(void* handle, size_t* len) {
+  std::ostringstream out;
+  hlm::write_hgr(*static_cast<hlm::Hypergraph*>(handle), out);
+  return dup_text(out.str(), len);
+}
+
+char* ref_write_matching(const uint32_t* matched, uint64_t count, double total_weight, uint32_t rounds, size_t* len) {
+  hlm::Matching m;
+  m.matched_edges.assign(matched, matched + count);
+  m.total_weight = total_weight;
+  m.rounds_used = rounds;
+  std::ostringstream out;
+  hlm::write_matching(m, out);
+  return dup_text(out.str(), len);
+}
+
+int ref_parse_matching(const char* text, size_t len, uint32_t** ids, uint64_t* count) {
+  try {
+    std::istringstream in(std::string(text, len));
+    const std::vector<hlm::edge_id> v = hlm::parse_matching(in);
+    *ids = dup_array(v);
+    *count = v.size();
+    return ORC_OK;
+  } catch (const hlm::input_error&) {
+    return ORC_INPUT_ERROR;
+  }
+}
+
+void ref_free_text(void* p) { std::free(p); }
+
 void ref_free_graph(orc_owned_graph* g) {
   std::free(g->vertex_offsets);
   std::free(g->vertex_incidence);

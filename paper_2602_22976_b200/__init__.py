@@ -21,8 +21,14 @@ from .api import (  # noqa: F401
     WorkCounters,
     default_max_rounds,
     eval_stream,
+    load_instance_file,
     local_max_crcw,
     local_max_crew,
+    parse_hgr,
+    parse_matching,
+    parse_metis_graph,
     run_variant,
     verify_matching,
+    write_hgr,
+    write_matching,
 )

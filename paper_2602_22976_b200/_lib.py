@@ -64,6 +64,13 @@ class MgSetup(C.Structure):
                 ("non_integer", C.c_int32), ("num_edges_global", C.c_uint32)]
 
 
+class HostGraph(C.Structure):
+    _fields_ = [("num_vertices", C.c_uint32), ("num_edges", C.c_uint32),
+                ("vertex_offsets", C.POINTER(C.c_uint64)), ("vertex_incidence", C.POINTER(C.c_uint32)),
+                ("edge_offsets", C.POINTER(C.c_uint64)), ("edge_members", C.POINTER(C.c_uint32)),
+                ("base_weights", C.POINTER(C.c_double)), ("num_warnings", C.c_uint32)]
+
+
 # every symbol include/hlm_b200.h declares: (restype, argtypes)
 SYMBOLS = {
     "hlm_b200_abi_version": (C.c_int, []),
@@ -94,6 +101,14 @@ SYMBOLS = {
     "hlm_b200_mg_exact_level": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hlm_b200_mg_end_round": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_int)]),
     "hlm_b200_mg_finish": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(Result)]),
+    "hlm_b200_parse_hgr": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
+    "hlm_b200_parse_metis_graph": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
+    "hlm_b200_host_graph_free": (None, [C.POINTER(HostGraph)]),
+    "hlm_b200_write_hgr": (C.c_int, [C.POINTER(CsrView), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "hlm_b200_write_matching": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, C.c_uint32, C.POINTER(C.c_void_p),
+                                          C.POINTER(C.c_size_t)]),
+    "hlm_b200_parse_matching": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "hlm_b200_text_free": (None, [C.c_void_p]),
 }
 
 _lib = None

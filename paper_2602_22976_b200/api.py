@@ -391,3 +391,93 @@ def eval_stream(stream: WeightStream, edges, rounds, base=None, device: int = 0)
     if st != _lib.OK:
         _raise(st, "hlm_b200_eval_stream")
     return w, t
+
+
+# ---- text formats (io.hpp of the reference), parsed / written on the host by the library ----------
+DEGREE_ZERO = {"reject": 0, "drop_and_renumber": 1, "drop": 1}
+
+
+def _take_host_graph(hg: _lib.HostGraph) -> Hypergraph:
+    n, m = int(hg.num_vertices), int(hg.num_edges)
+    kappa = int(hg.edge_offsets[m]) if m else 0
+    try:
+        return Hypergraph(n, m, _take(hg.vertex_offsets, n + 1, np.uint64), _take(hg.vertex_incidence, kappa, np.uint32),
+                          _take(hg.edge_offsets, m + 1, np.uint64), _take(hg.edge_members, kappa, np.uint32),
+                          _take(hg.base_weights, m, np.float64))
+    finally:
+        _lib.load_library().hlm_b200_host_graph_free(C.byref(hg))
+
+
+def _parse(fn_name: str, text, degree_zero: str, warnings: Optional[list]) -> Hypergraph:
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    hg = _lib.HostGraph()
+    st = getattr(_lib.load_library(), fn_name)(data, len(data), DEGREE_ZERO[degree_zero], C.byref(hg))
+    if st != _lib.OK:
+        _raise(st, fn_name)
+    if warnings is not None and hg.num_warnings:
+        warnings.append("vertex weights present but ignored; matching does not use them")
+    return _take_host_graph(hg)
+
+
+def parse_hgr(text, degree_zero: str = "reject", warnings: Optional[list] = None) -> Hypergraph:
+    """parse_hgr (io.hpp:79-137): hMetis .hgr text -> Hypergraph; raises InputError like the reference."""
+    return _parse("hlm_b200_parse_hgr", text, degree_zero, warnings)
+
+
+def parse_metis_graph(text, degree_zero: str = "reject") -> Hypergraph:
+    """parse_metis_graph (io.hpp:176-231): METIS graph text -> 2-uniform Hypergraph."""
+    return _parse("hlm_b200_parse_metis_graph", text, degree_zero, None)
+
+
+def _text_out(st: int, what: str, ptr: C.c_void_p, length: C.c_size_t) -> str:
+    if st != _lib.OK:
+        _raise(st, what)
+    try:
+        return C.string_at(ptr.value, length.value).decode()
+    finally:
+        _lib.load_library().hlm_b200_text_free(ptr)
+
+
+def write_hgr(h: Hypergraph) -> str:
+    """write_hgr (io.hpp:146-171): weights in shortest round-trip form, integral ones as integers."""
+    keep: list = []
+    view = _view(h, keep)
+    ptr, length = C.c_void_p(), C.c_size_t()
+    st = _lib.load_library().hlm_b200_write_hgr(C.byref(view), C.byref(ptr), C.byref(length))
+    return _text_out(st, "hlm_b200_write_hgr", ptr, length)
+
+
+def write_matching(m: Matching) -> str:
+    """write_matching (io.hpp:240-247)."""
+    ids = np.ascontiguousarray(m.matched_edges, dtype=np.uint32)
+    ptr, length = C.c_void_p(), C.c_size_t()
+    st = _lib.load_library().hlm_b200_write_matching(ids.ctypes.data if ids.size else None, ids.size,
+                                                      float(m.total_weight), int(m.rounds_used), C.byref(ptr),
+                                                      C.byref(length))
+    return _text_out(st, "hlm_b200_write_matching", ptr, length)
+
+
+def parse_matching(text) -> np.ndarray:
+    """parse_matching (io.hpp:249-257): edge ids, one or more per content line."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    ptr, count = C.c_void_p(), C.c_uint64()
+    lib = _lib.load_library()
+    st = lib.hlm_b200_parse_matching(data, len(data), C.byref(ptr), C.byref(count))
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_parse_matching")
+    try:
+        if count.value == 0:
+            return np.zeros(0, dtype=np.uint32)
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint32)), shape=(count.value,)).copy()
+    finally:
+        lib.hlm_b200_text_free(ptr)
+
+
+def load_instance_file(path: str, metis: bool = False, degree_zero: str = "reject") -> Hypergraph:
+    """load_instance_file (io.hpp:259-264)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError as exc:
+        raise IOError(f"cannot open instance file {path}") from exc  # hlm::io_error
+    return parse_metis_graph(data, degree_zero) if metis else parse_hgr(data, degree_zero)
