@@ -40,7 +40,9 @@ enum { HLM_B200_MODE_PERTURB_BASE = 0, HLM_B200_MODE_REPLACE_UNIFORM = 1 };
  * kernels.  SEQ and WORK_OPTIMAL are accepted and executed by the CRCW kernels (all variants return
  * the same matching by contract, tests/test_par.cpp:32-55; the CRCW path already compacts its
  * active lists every round, which is what work_optimal is for); their WorkCounters follow the
- * reference's own per-variant formulas.  GREEDY (a different, sequential algorithm) is not. */
+ * reference's own per-variant formulas.  GREEDY (greedy_sorted, local_max_seq.hpp:130) is the
+ * lexicographically first maximal matching under (weight descending, id ascending): it runs on the
+ * exact three-level path with that static order as the key and reports like the reference does. */
 enum {
   HLM_B200_VARIANT_SEQ = 0,
   HLM_B200_VARIANT_CRCW = 1,

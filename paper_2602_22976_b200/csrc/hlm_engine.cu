@@ -1013,7 +1013,13 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
 }
 
 int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
-  const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
+  // greedy_sorted (local_max_seq.hpp:130-152) is the lexicographically first maximal matching under
+  // the static order (weight descending, id ascending).  Repeating "every edge that is first in
+  // that order among its live neighbours is taken" reaches exactly that matching, so the variant
+  // runs on the exact three-level path with a static key; the rounds it needs (the dependency
+  // depth of the order) are an implementation detail, the reference reports one round.
+  const bool greedy = cfg->variant == HLM_B200_VARIANT_GREEDY;
+  const uint32_t max_rounds = greedy ? 65000u : (cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m));
   if (max_rounds > 65000u) {
     set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
     return HLM_B200_ERR_UNSUPPORTED;
@@ -1027,6 +1033,10 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   Launcher L;
   ST_CHECK(setup_launcher(g, st, cfg, max_rounds, L, nullptr, false));
   RoundParams& P = L.P;
+  if (greedy) {
+    L.exact = true;
+    P.greedy = 1u;
+  }
 
   bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact;
   if (use_graph && (!w.graph_exec[0] || !same_params(w.graph_key, P))) {
@@ -1152,6 +1162,10 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   int rc = assemble_result(g, rounds, cfg, cfg->variant, out);
   tr.mark("match: result");
   if (rc != HLM_B200_OK) return rc;
+  if (greedy && c.status == ST_ROUND_LIMIT) {
+    set_error("greedy: the dependency depth of the (weight, id) order exceeds %u rounds", max_rounds);
+    return HLM_B200_ERR_UNSUPPORTED;
+  }
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
 
@@ -1252,6 +1266,36 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     }
   }
   out->total_weight = tw;
+  if (variant == HLM_B200_VARIANT_GREEDY) {
+    // the reference's report for greedy (local_max_par.hpp:599-610): one round holding everything,
+    // and total_weight accumulated in scan order = (weight descending, id ascending)
+    if (need_w && total) {
+      const double* wts = static_cast<const double*>(w.pin_w);
+      std::vector<uint64_t> order(total);
+      for (uint64_t i = 0; i < total; ++i) order[i] = i;
+      std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+        if (wts[a] != wts[b]) return wts[a] > wts[b];
+        return out->matched_edges[a] < out->matched_edges[b];
+      });
+      double sum = 0.0;
+      for (uint64_t i : order) sum += wts[i];
+      out->total_weight = sum;
+    }
+    std::free(out->per_round_matched);
+    std::free(out->per_round_deactivated);
+    out->per_round_matched = static_cast<uint32_t*>(std::calloc(2, sizeof(uint32_t)));
+    out->per_round_deactivated = static_cast<uint32_t*>(std::calloc(2, sizeof(uint32_t)));
+    if (!out->per_round_matched || !out->per_round_deactivated) return HLM_B200_ERR_NOMEM;
+    out->per_round_matched[0] = static_cast<uint32_t>(total);
+    out->per_round_deactivated[0] = m - static_cast<uint32_t>(total);
+    out->rounds = 1;
+    if (out->matched_round)
+      for (uint64_t i = 0; i < total; ++i) out->matched_round[i] = 1;
+    out->total_edge_visits = m;
+    out->total_pin_visits = g->kappa;
+    out->write_conflicts = 0;
+    return HLM_B200_OK;
+  }
   // WorkCounters by the reference's per-variant formulas.  Soft-deletion variants charge the full
   // structure every round: seq 3m / 3k (local_max_seq.hpp:45-48,104), crcw 3m / 3k
   // (local_max_par.hpp:135,159,164,224,248), crew 5m / 4k (:135,159,164,285,299,320-321).
@@ -1302,9 +1346,11 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
     case HLM_B200_VARIANT_CREW:
       rc = match_crew(g, st, cfg, out);
       break;
-    case HLM_B200_VARIANT_GREEDY:
-      set_error("variant greedy (a sequential baseline, local_max_seq.hpp:130) is not implemented on the device");
-      return HLM_B200_ERR_UNSUPPORTED;
+    case HLM_B200_VARIANT_GREEDY: {  // run_variant's greedy branch (local_max_par.hpp:597-612): no stream
+      hlm_b200_stream none = {0, HLM_B200_GEN_XORSHIFT, HLM_B200_MODE_PERTURB_BASE, 0.0, 0.0};
+      rc = match_crcw(g, &none, cfg, out);
+      break;
+    }
     default:
       set_error("unknown variant %d", cfg->variant);  // local_max_par.hpp:615
       return HLM_B200_ERR_INPUT;

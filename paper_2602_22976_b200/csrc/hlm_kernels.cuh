@@ -872,10 +872,12 @@ __global__ void __launch_bounds__(kBlock) k_exact_level(const RoundParams P, con
       continue;
     }
     const uint32_t* __restrict__ pp = P.csr.pins + b;
-    const unsigned long long A = static_cast<unsigned long long>(
-        __double_as_longlong(edge_weight(P.stream, edge_gid(P, e), r, base_of(P, e))));
-    const unsigned long long B = tie_hash(P.stream, edge_gid(P, e), r);
-    const uint32_t C = edge_gid(P, e) + 1u;
+    // (A, B, C) ascending = the reference comparator (weight, tie_hash, id); for the greedy variant
+    // the static order of greedy_sorted: heavier first, then the LOWER id (local_max_seq.hpp:133-136)
+    const unsigned long long A = static_cast<unsigned long long>(__double_as_longlong(
+        P.greedy ? base_of(P, e) : edge_weight(P.stream, edge_gid(P, e), r, base_of(P, e))));
+    const unsigned long long B = P.greedy ? 0ull : tie_hash(P.stream, edge_gid(P, e), r);
+    const uint32_t C = P.greedy ? 0xFFFFFFFFu - edge_gid(P, e) : edge_gid(P, e) + 1u;
     bool win = true;
     for (uint32_t i = lane; i < s; i += 32) {
       const uint32_t v = __ldg(pp + i);

@@ -99,6 +99,8 @@ struct RoundParams {
   uint32_t* vtop;            // n: high word of vkey, or kTopDead; the L2-resident filter array
   uint32_t* dead;            // n bits: where completion marking sets its bits (multi-GPU: the exchange area)
   const uint32_t* dead_all;  // n bits: every vertex covered so far; stable during a sweep
+  uint32_t greedy;           // exact levels compare (base weight, lower id): the static priority of
+                             // greedy_sorted (local_max_seq.hpp:130-139) instead of the round's stream
   uint32_t hot_vtop;         // vertex ids below this keep their filter word in L1 (ld.ca); others ld.cg
   uint32_t hot_bits;         // same for the dead bitmap
   uint32_t dead_first;       // sweeps of rounds >= 2 test the bitmap (n/8 bytes, L2-resident) before

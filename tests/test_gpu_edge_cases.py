@@ -89,8 +89,6 @@ def test_input_errors(hb, port):
         _run(hb, g, po.Stream(noise_low=2.0, noise_high=1.0), "crew")
     with pytest.raises(hb.InputError):  # local_max_par.hpp:615
         hb.run_variant(to_hb_graph(g), hb.WeightStream(), hb.ParallelConfig(variant=7))
-    with pytest.raises(NotImplementedError):
-        hb.run_variant(to_hb_graph(g), hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
     bad = to_hb_graph(g)
     bad.edge_members = np.array([0, 1, 1, 9], dtype=np.uint32)  # vertex id out of range
     with pytest.raises(hb.InputError):

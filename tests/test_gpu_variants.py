@@ -61,3 +61,54 @@ def test_work_optimal_round_cap(hb, port):
     with pytest.raises(hb.RoundLimitError) as ei:
         hb.run_variant(to_hb_graph(g), to_hb_stream(s), hb.ParallelConfig(variant="work_optimal", max_rounds=2))
     assert list(ei.value.partial.matched_edges) == list(want.matched_edges)
+
+
+def test_greedy_variant_equals_greedy_sorted(hb, port, ref):
+    """run_variant(Variant::greedy) (local_max_par.hpp:597-612 -> greedy_sorted, local_max_seq.hpp:130):
+    the device reaches the same matching by iterating the static (weight desc, id asc) order to its
+    fixpoint; matched set, total weight (summed in scan order), the one-round report and the work
+    counters must equal the reference's."""
+    import numpy as np
+
+    rng = np.random.default_rng(3)
+    cases = list(_instances(port))
+    g = port.generate_random(3000, 5000, 2, 4, 21)
+    g.base_weights = rng.random(g.m) * 10 + 0.1          # real weights: the FP sum order matters
+    cases.append(("real weights", g))
+    g = port.generate_random(3000, 5000, 2, 4, 22)
+    g.base_weights = rng.integers(1, 4, g.m).astype(np.float64)  # heavy ties: decided by the lower id
+    cases.append(("three weight classes", g))
+    g = po.graph_from_edge_lists([[i, i + 1] for i in range(300)])  # unit path: dependency depth 150
+    cases.append(("unit path", g))
+    for name, g in cases:
+        want = ref.local_max(g, po.Stream(), variant=po.VARIANT_GREEDY)
+        got = hb.run_variant(to_hb_graph(g), hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
+        assert_same_result(got, want, f"greedy {name}")
+        assert got.report.rounds == 1 and got.report.work.rounds == 1
+        assert got.report.work.total_edge_visits == want.edge_visits == g.m
+        assert got.report.work.total_pin_visits == want.pin_visits == g.kappa
+        with hb.DeviceHypergraph.upload(to_hb_graph(g)) as dg:  # resident (renumbered, sorted) instance
+            again = dg.match(hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
+            assert_same_result(again, want, f"greedy resident {name}")
+            v = dg.verify(again.matching.matched_edges)
+            assert v.disjoint and v.maximal
+
+
+def test_quality_band_vs_greedy_acceptance_criterion_7(hb, port):
+    """acceptance.cpp:261-289 on the device: 100 instances (m = 50 .. 10^4, integer weights 1-100,
+    default [0,100) noise): geometric mean of crcw weight / greedy weight >= 0.85."""
+    import math
+
+    logs, worst = 0.0, 1.0
+    for i in range(100):
+        m = int(50.0 * 10.0 ** (2.30103 * i / 99.0))
+        g = port.generate_random(max(6, m), m, 2, 2 if i % 2 == 0 else 5, 80000 + i)
+        g.base_weights = port.random_weights_1_100(g.m, 7 * i + 1)
+        h = to_hb_graph(g)
+        crcw = hb.run_variant(h, hb.WeightStream(seed=300 + i), hb.ParallelConfig(variant="crcw"))
+        greedy = hb.run_variant(h, hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
+        ratio = crcw.matching.total_weight / greedy.matching.total_weight
+        logs += math.log(ratio)
+        worst = min(worst, ratio)
+    geomean = math.exp(logs / 100)
+    assert geomean >= 0.85, (geomean, worst)
