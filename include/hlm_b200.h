@@ -255,6 +255,21 @@ int hlm_b200_write_matching(const uint32_t* matched, uint64_t count, double tota
 int hlm_b200_parse_matching(const char* text, size_t len, uint32_t** ids, uint64_t* count);
 void hlm_b200_text_free(void* p); /* texts and id arrays returned by the three calls above */
 
+/* compact (local_max_par.hpp:350-454) on the device: both CSRs rebuilt over the active vertices and
+ * edges (dense, order-preserving renumbering by exclusive scans over the flags); active vertices
+ * left without an active edge are dropped.  *vertex_map / *edge_map: old id -> new id or 0xFFFFFFFF
+ * (release with hlm_b200_text_free).  An active edge touching an inactive vertex is
+ * HLM_B200_ERR_INPUT (the reference's input_error).  `work`, if given, receives what the reference
+ * adds to its WorkCounters for one compaction (:446-453). */
+typedef struct {
+  uint64_t total_edge_visits;
+  uint64_t total_pin_visits;
+  uint32_t prefix_sum_invocations;
+  uint32_t compactions;
+} hlm_b200_compact_work;
+int hlm_b200_compact(const hlm_b200_csr_view* h, const uint8_t* vertex_active, const uint8_t* edge_active, int device,
+                     hlm_b200_host_graph* out, uint32_t** vertex_map, uint32_t** edge_map, hlm_b200_compact_work* work);
+
 /* default_max_rounds (matching.hpp:87-89). */
 uint32_t hlm_b200_default_max_rounds(uint32_t num_edges);
 

@@ -339,6 +339,28 @@ class Oracle:
         self._fn("free_text", None, [C.c_void_p])(C.cast(ptr, C.c_void_p))
         return rc, out
 
+    def compact(self, g: Graph, vertex_active, edge_active, workers: int = 2):
+        """reference only: (status, Graph, vertex_map, edge_map, [edge visits, pin visits, scans, compactions])"""
+        assert self.kind == "reference"
+        va = np.ascontiguousarray(vertex_active, dtype=np.uint8)
+        ea = np.ascontiguousarray(edge_active, dtype=np.uint8)
+        vmap, emap = np.empty(g.n, dtype=np.uint32), np.empty(g.m, dtype=np.uint32)
+        counters = np.zeros(4, dtype=np.uint64)
+        og = COwnedGraph()
+        h = self.graph_handle(g)
+        try:
+            f = self._fn("compact", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p])
+            rc = f(h, va.ctypes.data, ea.ctypes.data, workers, C.addressof(og), vmap.ctypes.data, emap.ctypes.data,
+                   counters.ctypes.data)
+        finally:
+            self.graph_release(h)
+        if rc != OK:
+            return rc, None, None, None, None
+        out = _own_graph(og)
+        self._fn("free_graph", None, [C.c_void_p])(C.addressof(og))
+        return rc, out, vmap, emap, counters.tolist()
+
     def hardware_workers(self) -> int:
         if self.kind == "reference":
             return int(self._fn("hardware_workers", C.c_uint, [])())

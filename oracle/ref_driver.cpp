@@ -251,6 +251,29 @@ int ref_parse_matching(const char* text, size_t len, uint32_t** ids, uint64_t* c
 
 void ref_free_text(void* p) { std::free(p); }
 
+// compact (local_max_par.hpp:350-454): vmap / emap are caller arrays of n / m entries; counters[4] =
+// {edge visits, pin visits, prefix sums, compactions} added by this one call
+int ref_compact(void* handle, const uint8_t* vact, const uint8_t* eact, unsigned workers, orc_owned_graph* out,
+                uint32_t* vmap, uint32_t* emap, uint64_t* counters) {
+  std::memset(out, 0, sizeof(*out));
+  const auto& h = *static_cast<hlm::Hypergraph*>(handle);
+  try {
+    hlm::WorkCounters wc;
+    hlm::CompactResult c = hlm::compact(h, std::span<const std::uint8_t>(vact, h.num_vertices),
+                                        std::span<const std::uint8_t>(eact, h.num_edges), workers, &wc);
+    export_graph(c.graph, out);
+    if (h.num_vertices) std::memcpy(vmap, c.vertex_map.data(), sizeof(uint32_t) * h.num_vertices);
+    if (h.num_edges) std::memcpy(emap, c.edge_map.data(), sizeof(uint32_t) * h.num_edges);
+    counters[0] = wc.total_edge_visits;
+    counters[1] = wc.total_pin_visits;
+    counters[2] = wc.prefix_sum_invocations;
+    counters[3] = wc.compactions;
+    return ORC_OK;
+  } catch (const hlm::input_error&) {
+    return ORC_INPUT_ERROR;
+  }
+}
+
 void ref_free_graph(orc_owned_graph* g) {
   std::free(g->vertex_offsets);
   std::free(g->vertex_incidence);

@@ -18,7 +18,9 @@ from .api import (  # noqa: F401
     RunReport,
     VerificationReport,
     WeightStream,
+    CompactResult,
     WorkCounters,
+    compact,
     default_max_rounds,
     eval_stream,
     load_instance_file,

@@ -71,6 +71,11 @@ class HostGraph(C.Structure):
                 ("base_weights", C.POINTER(C.c_double)), ("num_warnings", C.c_uint32)]
 
 
+class CompactWork(C.Structure):
+    _fields_ = [("total_edge_visits", C.c_uint64), ("total_pin_visits", C.c_uint64),
+                ("prefix_sum_invocations", C.c_uint32), ("compactions", C.c_uint32)]
+
+
 # every symbol include/hlm_b200.h declares: (restype, argtypes)
 SYMBOLS = {
     "hlm_b200_abi_version": (C.c_int, []),
@@ -109,6 +114,8 @@ SYMBOLS = {
                                           C.POINTER(C.c_size_t)]),
     "hlm_b200_parse_matching": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
     "hlm_b200_text_free": (None, [C.c_void_p]),
+    "hlm_b200_compact": (C.c_int, [C.POINTER(CsrView), C.c_void_p, C.c_void_p, C.c_int, C.POINTER(HostGraph),
+                                   C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(CompactWork)]),
 }
 
 _lib = None

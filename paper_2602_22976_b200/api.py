@@ -481,3 +481,37 @@ def load_instance_file(path: str, metis: bool = False, degree_zero: str = "rejec
     except OSError as exc:
         raise IOError(f"cannot open instance file {path}") from exc  # hlm::io_error
     return parse_metis_graph(data, degree_zero) if metis else parse_hgr(data, degree_zero)
+
+
+@dataclass
+class CompactResult:
+    """CompactResult (local_max_par.hpp:340-344) plus what one compaction adds to the WorkCounters."""
+    graph: Hypergraph
+    vertex_map: np.ndarray  # old id -> new id or 0xFFFFFFFF
+    edge_map: np.ndarray
+    work: WorkCounters
+
+
+def compact(h: Hypergraph, vertex_active, edge_active, device: int = 0) -> CompactResult:
+    """compact (local_max_par.hpp:350-454) on the device; needs both CSR sides of `h`."""
+    lib = _lib.load_library()
+    keep: list = []
+    view = _view(h, keep)
+    va = np.ascontiguousarray(vertex_active, dtype=np.uint8)
+    ea = np.ascontiguousarray(edge_active, dtype=np.uint8)
+    if va.size != h.num_vertices or ea.size != h.num_edges:
+        raise InputError("activity flag arrays do not match the hypergraph")
+    hg, vm, em, wk = _lib.HostGraph(), C.c_void_p(), C.c_void_p(), _lib.CompactWork()
+    st = lib.hlm_b200_compact(C.byref(view), va.ctypes.data if va.size else None, ea.ctypes.data if ea.size else None,
+                              device, C.byref(hg), C.byref(vm), C.byref(em), C.byref(wk))
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_compact")
+    try:
+        vmap = _take(C.cast(vm, C.POINTER(C.c_uint32)), h.num_vertices, np.uint32)
+        emap = _take(C.cast(em, C.POINTER(C.c_uint32)), h.num_edges, np.uint32)
+    finally:
+        lib.hlm_b200_text_free(vm)
+        lib.hlm_b200_text_free(em)
+    return CompactResult(_take_host_graph(hg), vmap, emap,
+                         WorkCounters(0, int(wk.total_edge_visits), int(wk.total_pin_visits),
+                                      int(wk.prefix_sum_invocations), int(wk.compactions)))

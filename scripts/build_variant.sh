@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 name=$1; shift
 out=build/variants; mkdir -p $out/$name
 FLAGS="-gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 -fmad=false"
-for f in hlm_engine hlm_loader hlm_crew hlm_io; do
+for f in hlm_engine hlm_loader hlm_crew hlm_io hlm_compact; do
   nvcc $FLAGS "$@" -c paper_2602_22976_b200/csrc/$f.cu -o $out/$name/$f.o &
 done
 wait
