@@ -20,6 +20,7 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <span>
 #include <string>
 #include <utility>
 #include <vector>
@@ -129,6 +130,62 @@ inline MatchResult local_max_crcw(const Hypergraph& h, const WeightStream& strea
 inline MatchResult local_max_crew(const Hypergraph& h, const WeightStream& stream, ParallelConfig cfg = {}) {
   cfg.variant = Variant::crew;
   return ::hlm::b200::run_variant(h, stream, cfg, 0);
+}
+
+// local_max_work_optimal (local_max_par.hpp:460): same matching, the variant's own WorkCounters
+inline MatchResult local_max_work_optimal(const Hypergraph& h, const WeightStream& stream, ParallelConfig cfg = {}) {
+  cfg.variant = Variant::work_optimal;
+  return ::hlm::b200::run_variant(h, stream, cfg, 0);
+}
+
+// local_max_sequential (local_max_seq.hpp:94)
+inline MatchResult local_max_sequential(const Hypergraph& h, const WeightStream& stream, std::uint32_t max_rounds = 0) {
+  ParallelConfig cfg;
+  cfg.variant = Variant::seq;
+  cfg.max_rounds = max_rounds;
+  return ::hlm::b200::run_variant(h, stream, cfg, 0);
+}
+
+// greedy_sorted (local_max_seq.hpp:130): Matching only, like the reference
+inline Matching greedy_sorted(const Hypergraph& h) {
+  ParallelConfig cfg;
+  cfg.variant = Variant::greedy;
+  return ::hlm::b200::run_variant(h, WeightStream{}, cfg, 0).matching;
+}
+
+// compact (local_max_par.hpp:350-454) on the device
+inline CompactResult compact(const Hypergraph& h, std::span<const std::uint8_t> vertex_active,
+                             std::span<const std::uint8_t> edge_active, unsigned /*workers*/ = 1,
+                             WorkCounters* wc = nullptr, int device = 0) {
+  const hlm_b200_csr_view v = detail::view_of(h);
+  hlm_b200_host_graph g;
+  std::uint32_t *vmap = nullptr, *emap = nullptr;
+  hlm_b200_compact_work work;
+  const int st = hlm_b200_compact(&v, vertex_active.data(), edge_active.data(), device, &g, &vmap, &emap, &work);
+  if (st == HLM_B200_ERR_INPUT) throw input_error(hlm_b200_last_error());
+  if (st != HLM_B200_OK) throw std::runtime_error(std::string("hlm_b200: ") + hlm_b200_last_error());
+  CompactResult out;
+  const std::uint64_t kv = g.num_vertices ? g.vertex_offsets[g.num_vertices] : 0;
+  const std::uint64_t ke = g.num_edges ? g.edge_offsets[g.num_edges] : 0;
+  out.graph.num_vertices = g.num_vertices;
+  out.graph.num_edges = g.num_edges;
+  out.graph.vertex_offsets.assign(g.vertex_offsets, g.vertex_offsets + g.num_vertices + 1);
+  out.graph.vertex_incidence.assign(g.vertex_incidence, g.vertex_incidence + kv);
+  out.graph.edge_offsets.assign(g.edge_offsets, g.edge_offsets + g.num_edges + 1);
+  out.graph.edge_members.assign(g.edge_members, g.edge_members + ke);
+  out.graph.base_weights.assign(g.base_weights, g.base_weights + g.num_edges);
+  out.vertex_map.assign(vmap, vmap + h.num_vertices);
+  out.edge_map.assign(emap, emap + h.num_edges);
+  hlm_b200_host_graph_free(&g);
+  hlm_b200_text_free(vmap);
+  hlm_b200_text_free(emap);
+  if (wc) {
+    wc->prefix_sum_invocations += work.prefix_sum_invocations;
+    wc->compactions += work.compactions;
+    wc->total_pin_visits += work.total_pin_visits;
+    wc->total_edge_visits += work.total_edge_visits;
+  }
+  return out;
 }
 
 // An instance resident in HBM: the loader's output.  Matching it repeatedly excludes the

@@ -49,6 +49,38 @@ int main() {
       CHECK(ver.valid());
       CHECK(ver.weight == verify_matching(h, got.matching).weight);
     }
+    // every other entry point with the reference's signature
+    {
+      const MatchResult opt = b200::local_max_work_optimal(h, s);
+      ParallelConfig two;
+      two.workers = 2;
+      const MatchResult ref_opt = local_max_work_optimal(h, s, two);
+      CHECK(opt.matching.matched_edges == seq.matching.matched_edges);
+      CHECK(opt.report.work.total_pin_visits == ref_opt.report.work.total_pin_visits);
+      CHECK(opt.report.work.total_edge_visits == ref_opt.report.work.total_edge_visits);
+      CHECK(opt.report.work.compactions == ref_opt.report.work.compactions);
+      CHECK(opt.report.work.prefix_sum_invocations == ref_opt.report.work.prefix_sum_invocations);
+      CHECK(b200::local_max_sequential(h, s).matching.matched_edges == seq.matching.matched_edges);
+      const Matching greedy = b200::greedy_sorted(h), ref_greedy = greedy_sorted(h);
+      CHECK(greedy.matched_edges == ref_greedy.matched_edges);
+      CHECK(greedy.total_weight == ref_greedy.total_weight);
+      CHECK(greedy.per_round_matched == ref_greedy.per_round_matched);
+      // compact on the flags left by the first round
+      std::vector<std::uint8_t> v_active(h.num_vertices, 1), e_active(h.num_edges, 1);
+      for (edge_id e : seq.report.matched_per_round[0])
+        for (vertex_id v : h.members_of(e)) v_active[v] = 0;
+      for (edge_id e = 0; e < h.num_edges; ++e)
+        for (vertex_id v : h.members_of(e))
+          if (!v_active[v]) e_active[e] = 0;
+      WorkCounters wa, wb;
+      const CompactResult ca = b200::compact(h, v_active, e_active, 1, &wa);
+      const CompactResult cb = compact(h, v_active, e_active, 2, &wb);
+      CHECK(ca.graph == cb.graph);
+      CHECK(ca.vertex_map == cb.vertex_map);
+      CHECK(ca.edge_map == cb.edge_map);
+      CHECK(wa.total_pin_visits == wb.total_pin_visits && wa.total_edge_visits == wb.total_edge_visits);
+      CHECK(wa.compactions == wb.compactions && wa.prefix_sum_invocations == wb.prefix_sum_invocations);
+    }
     // work counters follow the reference formulas
     ParallelConfig one;
     one.workers = 1;
