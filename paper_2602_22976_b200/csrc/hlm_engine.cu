@@ -776,14 +776,13 @@ struct Launcher {
       // (measured, profiles/README.md)
       const int sgrid = g->num_sms * HLM_SIMPLE_MIN_BLOCKS;
       switch (g->uniform_d) {
-        // with keys: survivors queued per warp and processed 32 at a time (k_sweep_uniform_dense)
+        // d = 2 with keys: survivors queued per warp and processed 32 at a time (k_sweep_uniform_dense)
         case 2:
           if constexpr (VMAX) k_sweep_uniform_dense<2><<<sgrid, kBlock, 0, s>>>(P);
           else k_sweep_uniform_simple<2, false><<<sgrid, kBlock, 0, s>>>(P);
           break;
-        case 4:
-          if constexpr (VMAX) k_sweep_uniform_dense<4><<<sgrid, kBlock, 0, s>>>(P);
-          else k_sweep_uniform_simple<4, false><<<sgrid, kBlock, 0, s>>>(P);
+        case 4:  // the dense form spills with four pins per edge and measured 2 % slower
+          k_sweep_uniform_simple<4, VMAX><<<sgrid, kBlock, 0, s>>>(P);
           break;
         case 8: k_sweep_uniform<8, VMAX, false><<<grid, kBlock, 0, s>>>(P); break;
         default: k_filter_vmax_small<VMAX><<<g->round_grid, kBlock, 0, s>>>(P); break;
