@@ -949,6 +949,10 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
     L.exact = true;
     P.ks.tag_period = 65534u;
   }
+  P.ks.fast_default = (P.ks.kind == KEY_WEIGHT_BITS && P.stream.kind == HLM_B200_GEN_XORSHIFT &&
+                       P.stream.mode == HLM_B200_MODE_PERTURB_BASE && P.stream.width != 0.0)
+                          ? 1u
+                          : 0u;
   // the load-before-atomic filter pays off once a vertex sees many edges per round
   P.ks.precheck = (g->n && g->kappa / g->n >= 6) ? 1u : 0u;
   if (const char* env = std::getenv("HLM_B200_PRECHECK")) P.ks.precheck = env[0] == '1';

@@ -38,6 +38,7 @@ struct KeyScheme {
   int32_t hash_bits;     // KEY_INT_HASH only
   uint32_t tag_period;   // number of distinct non-zero tags = 2^(64-payload_bits) - 1 (capped)
   uint32_t precheck;     // filter atomics with a plain L2 load of the running maximum first
+  uint32_t fast_default; // xorshift + perturb_base + width != 0 + KEY_WEIGHT_BITS: branch-free key code
   uint64_t wmin_bits;    // KEY_WEIGHT_BITS: bits of the smallest possible weight
   uint64_t wq_min;       // KEY_INT_HASH: smallest integer weight
 };
@@ -98,6 +99,13 @@ __device__ __forceinline__ uint32_t round_tag(const KeyScheme& k, uint32_t r) {
 __device__ __forceinline__ uint64_t priority_key(const StreamParams& s, const KeyScheme& k,
                                                  uint32_t e, uint32_t r, double base, uint32_t tag) {
   uint64_t payload;
+  if (k.fast_default) {
+    // the reference's default stream (xorshift noise added to the base weight, non-zero width,
+    // weight-bit keys) as straight-line code: same operations, no branches on the stream's fields
+    const double u = unit_from_bits(mix_xorshift(stream_counter(s, e, r)));
+    const double w = __dadd_rn(__dadd_rn(base, s.lo), __dmul_rn(u, s.width));
+    return (static_cast<uint64_t>(tag) << k.payload_bits) | (static_cast<uint64_t>(__double_as_longlong(w)) - k.wmin_bits);
+  }
   const double w = edge_weight(s, e, r, base);
   if (k.kind == KEY_WEIGHT_BITS) {
     payload = static_cast<uint64_t>(__double_as_longlong(w)) - k.wmin_bits;
