@@ -1019,6 +1019,7 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
     P.large_chunk *= 2u;
   // candidate lists are short: claim several regions per ticket, but keep every resident warp busy
   P.check_claim = std::min<uint32_t>(kCoarseClaim, std::max<uint32_t>(1u, P.nseg / (static_cast<uint32_t>(g->check_grid) * kWarpsPerBlock)));
+  if (const char* env = std::getenv("HLM_B200_CHECK_CLAIM")) P.check_claim = std::max(1, std::min(8, std::atoi(env)));
   return HLM_B200_OK;
 }
 
