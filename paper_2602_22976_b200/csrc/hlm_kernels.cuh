@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
 
 // Check + commit over the candidate lists (local_max_par.hpp:202-224): a candidate is matched iff
 // its key is the maximum at every pin; matched edges record their round and kill their pins.
-// A warp claims P.check_claim (<= kCoarseClaim) consecutive regions and walks the concatenation of their (short)
+// A warp claims P.check_claim (<= kCoarseClaim) regions and walks the concatenation of their (short)
 // candidate lists, kCheckItems candidates per lane and step, so that several independent chains
 // list id -> pins -> filter word are in flight per thread.
 constexpr int kCheckItems = 4;
@@ -680,11 +680,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   const uint32_t lane = threadIdx.x & 31;
   uint32_t local_matched = 0, local_mpins = 0;
 
+  // The regions of one claim are spread over the whole id space (ticket, ticket + stride, ...): on a
+  // sorted, degree-renumbered instance the candidate density grows steadily along the id space (hub
+  // regions hold almost none), and consecutive regions per claim left the last claims with all the work.
+  const uint32_t stride = (P.nseg + P.check_claim - 1u) / P.check_claim;
   for (uint32_t ticket = grid_warp();; ticket = claim_region(&c->ticket_c, lane, true)) {
-    const uint32_t seg0 = ticket * P.check_claim;
-    if (seg0 >= P.nseg) break;
-    // end[j] = candidates in regions seg0 .. seg0+j (inclusive prefix), the same in every lane
-    uint32_t mine = (lane < P.check_claim && seg0 + lane < P.nseg) ? list_cnt[seg0 + lane] : 0u;
+    if (ticket >= stride) break;
+    // end[j] = candidates in the first j+1 regions of the claim (inclusive prefix), the same in every lane
+    uint32_t mine = (lane < P.check_claim && ticket + lane * stride < P.nseg) ? list_cnt[ticket + lane * stride] : 0u;
 #pragma unroll
     for (int o = 1; o < static_cast<int>(kCoarseClaim); o <<= 1) {
       const uint32_t t = __shfl_up_sync(0xffffffffu, mine, o);
@@ -708,7 +711,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
             j = q + 1;
             begin = end[q];
           }
-        e[k] = valid[k] ? list[static_cast<size_t>(seg0 + j) * P.seg_cap + (idx - begin)] : 0u;
+        e[k] = valid[k] ? list[static_cast<size_t>(ticket + j * stride) * P.seg_cap + (idx - begin)] : 0u;
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
