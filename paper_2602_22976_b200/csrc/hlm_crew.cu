@@ -17,6 +17,7 @@
 // exact: ties are resolved inline, so there is no tie flag and no exact redo here.
 // Per-edge state is indexed by the caller's edge ids (the incidence lists name edges that way).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -50,6 +51,26 @@ struct CrewState {
   uint32_t* vlist[3] = {nullptr, nullptr, nullptr};  // light / mid / hub vertex ids
   uint32_t vcount[3] = {0, 0, 0};
   uint32_t* counters = nullptr;        // [0] matched this round, [1] deactivated this round
+  // ---- work-optimal form (crew2_*) ----
+  bool v2 = false;
+  uint32_t* winc = nullptr;    // kappa: incidence lists compacted in place, round after round
+  uint8_t* vw8 = nullptr;      // kappa: base weight of every incidence entry as a byte (integer weights 0..255)
+  uint8_t* ww8 = nullptr;      // kappa: the same, moving with winc
+  uint32_t* vlen = nullptr;    // n: live length of a light vertex's list (0: heavy, dead or isolated)
+  uint32_t* alive = nullptr;   // m bits, caller edge ids
+  uint32_t* votes = nullptr;   // m 16-bit lanes: vertices whose argmax is this edge, this round
+  uint32_t* vnew = nullptr;    // n bits: vertices covered in this round
+  uint32_t* inv = nullptr;     // m: caller id -> resident row (null: same order)
+  uint32_t num_heavy = 0, num_tasks = 0;
+  uint32_t* heavy_v = nullptr;      // heavy vertex ids
+  uint32_t* heavy_first = nullptr;  // first task of a heavy vertex
+  uint32_t* heavy_nt = nullptr;     // its number of tasks
+  uint32_t* task_hv = nullptr;      // task -> index into heavy_v
+  unsigned long long* task_begin = nullptr;  // first position of the task's chunk
+  uint32_t* task_len0 = nullptr;    // chunk length at the start
+  uint32_t* task_len = nullptr;     // live length
+  unsigned long long* part_key = nullptr;  // per task: best key of the chunk
+  uint32_t* part_id = nullptr;
 };
 
 struct CrewParams {
@@ -250,12 +271,30 @@ void crew_release(Graph* g) {
   pool_free(c->vdead);
   for (auto& l : c->vlist) pool_free(l);
   pool_free(c->counters);
+  pool_free(c->winc);
+  pool_free(c->vw8);
+  pool_free(c->ww8);
+  pool_free(c->vlen);
+  pool_free(c->alive);
+  pool_free(c->votes);
+  pool_free(c->vnew);
+  pool_free(c->inv);
+  pool_free(c->heavy_v);
+  pool_free(c->heavy_first);
+  pool_free(c->heavy_nt);
+  pool_free(c->task_hv);
+  pool_free(c->task_begin);
+  pool_free(c->task_len0);
+  pool_free(c->task_len);
+  pool_free(c->part_key);
+  pool_free(c->part_id);
   delete c;
   g->crew = nullptr;
 }
 
 static int crew_setup(Graph* g) {
-  if (g->crew) return HLM_B200_OK;
+  if (g->crew && !g->crew->v2) return HLM_B200_OK;
+  if (g->crew) crew_release(g);
   ST_CHECK(build_incidence(g));
   CrewState* c = new CrewState();
   g->crew = c;
@@ -277,7 +316,7 @@ static int crew_setup(Graph* g) {
   return HLM_B200_OK;
 }
 
-int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
   const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
   if (max_rounds > 65000u) {
     set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
@@ -361,6 +400,15 @@ int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   int rc = assemble_result(g, round, cfg, HLM_B200_VARIANT_CREW, out);
   if (rc != HLM_B200_OK) return rc;
   return limit ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
+}
+
+#include "hlm_crew2.inc"
+
+int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+  const char* env = std::getenv("HLM_B200_CREW_SOFT");
+  // 16-bit vote lanes: an edge with more pins than that takes the soft-deletion form
+  if ((env && env[0] == '1') || g->max_edge_size > 65535u) return match_crew_soft(g, st, cfg, out);
+  return match_crew_compacting(g, st, cfg, out);
 }
 
 }  // namespace hlmb

@@ -103,8 +103,24 @@ struct SweepSlot {
 template <int D>
 struct SweepState {
   uint32_t out_off, cand_off, local_deact;
+  uint32_t q_head, q_n;  // deposit queue of the warp (ring of kDepositRing entries)
   bool tie;
 };
+
+// Deposit queue (round 1): only a few percent of the pins still raise a vertex maximum, so a batch
+// issued its returning atomicMax with one or two active lanes and then waited for it -- half of the
+// stall samples of the round-1 sweep (profiles/ncu_c2_r01_final.md).  The (vertex, key) pairs that
+// need the atomic are queued per warp in shared memory and issued 32 at a time: one wait per 32
+// deposits instead of one per batch and pin.  A deposit may now happen later than its batch; the
+// filter words other warps read in the meantime are stale-low, which the pre-filter allows.
+constexpr uint32_t kDepositRing = 64;
+struct DepositQueue {
+  unsigned long long key[kDepositRing];
+  uint32_t v[kDepositRing];
+};
+#ifndef HLM_DEPOSIT_QUEUE
+#define HLM_DEPOSIT_QUEUE 1
+#endif
 
 template <int D, bool VMAX, bool R1>
 struct SweepCtx {
@@ -114,6 +130,23 @@ struct SweepCtx {
   const uint32_t* __restrict__ in;
   uint32_t* __restrict__ out;
   uint32_t seg_base, cnt;
+  DepositQueue* q;
+  static constexpr bool kQueue = R1 && HLM_DEPOSIT_QUEUE;
+
+  // issue the first `take` queued deposits, one per lane
+  __device__ __forceinline__ void flush(SweepState<D>& st, uint32_t take) const {
+    if (lane < take) {
+      const uint32_t slot = (st.q_head + lane) & (kDepositRing - 1u);
+      const unsigned long long key = q->key[slot];
+      const uint32_t v = q->v[slot];
+      const unsigned long long old = atomicMax(P.vkey + v, key);
+      atomicMax(P.vtop + v, static_cast<uint32_t>(key >> 32));
+      st.tie |= (old == key);
+    }
+    st.q_head += take;
+    st.q_n -= take;
+    __syncwarp();
+  }
 
   // one pipeline step: stage A on `a`, B on `b`, C1 on `c1`, C2 on `c2`
   __device__ __forceinline__ void step(uint32_t it, SweepSlot<D>& a, SweepSlot<D>& b, SweepSlot<D>& c1,
@@ -171,16 +204,36 @@ struct SweepCtx {
     // ---- stage C2: batch it-3
     if constexpr (VMAX) {
       bool cand = false;
+      unsigned long long key = 0ull;
+      uint32_t need = 0u;  // bit i: pin i still needs the atomic (queued form)
       if (c2.live) {
-        const unsigned long long key = priority_key(P.stream, P.ks, c2.oid + P.id_base, r, c2.base, tag);
+        key = priority_key(P.stream, P.ks, c2.oid + P.id_base, r, c2.base, tag);
         const uint32_t hi = static_cast<uint32_t>(key >> 32);
         bool lost = false;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          st.tie |= deposit_key(P, c2.pv.v[i], key, c2.cur[i]);
+          if constexpr (kQueue) need |= (c2.cur[i] > hi ? 0u : 1u) << i;
+          else st.tie |= deposit_key(P, c2.pv.v[i], key, c2.cur[i]);
           lost |= c2.cur[i] > hi;  // a larger key was already there: cannot win this round
         }
         cand = !lost;
+      }
+      if constexpr (kQueue) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const bool mine = (need >> i) & 1u;
+          const uint32_t nb = __ballot_sync(0xffffffffu, mine);
+          if (nb) {
+            if (mine) {
+              const uint32_t slot = (st.q_head + st.q_n + __popc(nb & lt_mask)) & (kDepositRing - 1u);
+              q->key[slot] = key;
+              q->v[slot] = c2.pv.v[i];
+            }
+            st.q_n += __popc(nb);
+            __syncwarp();
+            if (st.q_n >= 32u) flush(st, 32u);
+          }
+        }
       }
       // edges that may still win go to the (dense) candidate list of the check kernel
       const uint32_t ballot = __ballot_sync(0xffffffffu, cand);
@@ -198,9 +251,11 @@ struct SweepTuning {  // CTAs per SM = register budget of the four in-flight bat
 template <int D, bool VMAX, bool R1>
 __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_uniform(const RoundParams P) {
   static_assert(!R1 || VMAX, "round 1 without keys has nothing to do");
+  __shared__ DepositQueue s_queue[SweepCtx<D, VMAX, R1>::kQueue ? kWarpsPerBlock : 1];
   Ctrl* c = P.ctrl;
   const uint32_t par = c->parity;
   SweepCtx<D, VMAX, R1> X{P};
+  X.q = &s_queue[SweepCtx<D, VMAX, R1>::kQueue ? (threadIdx.x >> 5) : 0];
   X.r = c->round;
   X.tag = round_tag(P.ks, X.r);
   X.lane = threadIdx.x & 31;
@@ -216,6 +271,7 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   uint32_t local_kept = 0;
   SweepState<D> st;
   st.local_deact = 0;
+  st.q_head = st.q_n = 0;
   st.tie = false;
 
   const uint32_t gran = R1 ? 1u : claim_granularity(P, c->active_prev);
@@ -254,6 +310,9 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
       if (VMAX) P.cand_cnt[seg] = st.cand_off;
       local_kept += kept;
     }
+  }
+  if constexpr (SweepCtx<D, VMAX, R1>::kQueue) {
+    if (st.q_n) X.flush(st, st.q_n);
   }
   const uint32_t d = warp_sum(st.local_deact);
   if (X.lane == 0) {
