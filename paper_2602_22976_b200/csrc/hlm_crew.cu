@@ -17,6 +17,7 @@
 // exact: ties are resolved inline, so there is no tie flag and no exact redo here.
 // Per-edge state is indexed by the caller's edge ids (the incidence lists name edges that way).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>

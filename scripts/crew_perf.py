@@ -16,28 +16,32 @@ CASES = {
     "c3": dict(family="powerlaw", n=50_000_000, m=100_000_000, seed=1),
     "c2": dict(family="rmat", scale=24, m=1 << 28, seed=1, int_weights=True),
 }
-which = sys.argv[1:] or ["c1", "c2s", "c3s", "c4", "u8s"]
-for name in which:
-    dg = hb.DeviceHypergraph.generate(**CASES[name])
-    info = dg.info()
-    ref = None
-    for label, variant, soft in (("crcw", "crcw", "0"), ("crew", "crew", "0"), ("crew-soft", "crew", "1")):
-        if label == "crew-soft" and name in ("u8", "c3", "c2"):
-            continue
-        os.environ["HLM_B200_CREW_SOFT"] = soft
-        best = None
-        for _ in range(4):
-            r = dg.match(hb.WeightStream(), hb.ParallelConfig(variant=variant, loop_mode="graph"))
-            if best is None or r.report.device_ms < best.report.device_ms:
-                best = r
-        ids = np.asarray(best.matching.matched_edges)
-        if ref is None:
-            ref = (ids.copy(), best.report.rounds, list(best.report.matched_per_round_count), list(best.report.deactivated_per_round))
-            same = "ref"
-        else:
-            same = "same" if (np.array_equal(ids, ref[0]) and best.report.rounds == ref[1] and
-                              list(best.report.matched_per_round_count) == ref[2] and
-                              list(best.report.deactivated_per_round) == ref[3]) else "DIFFERENT"
-        print(f"{name:4s} {label:9s} pins {info.num_pins:11d} rounds {best.report.rounds:2d} |M| {len(ids):9d} "
-              f"device ms {best.report.device_ms:9.3f}  G pins/s {info.num_pins / best.report.device_ms / 1e6:7.2f}  {same}", flush=True)
-    dg.release()
+def main(which):
+  for name in which:
+      dg = hb.DeviceHypergraph.generate(**CASES[name])
+      info = dg.info()
+      ref = None
+      for label, variant, soft in (("crcw", "crcw", "0"), ("crew", "crew", "0"), ("crew-soft", "crew", "1")):
+          if label == "crew-soft" and name in ("u8", "c3", "c2"):
+              continue
+          os.environ["HLM_B200_CREW_SOFT"] = soft
+          best = None
+          for _ in range(4):
+              r = dg.match(hb.WeightStream(), hb.ParallelConfig(variant=variant, loop_mode="graph"))
+              if best is None or r.report.device_ms < best.report.device_ms:
+                  best = r
+          ids = np.asarray(best.matching.matched_edges)
+          if ref is None:
+              ref = (ids.copy(), best.report.rounds, list(best.report.matched_per_round_count), list(best.report.deactivated_per_round))
+              same = "ref"
+          else:
+              same = "same" if (np.array_equal(ids, ref[0]) and best.report.rounds == ref[1] and
+                                list(best.report.matched_per_round_count) == ref[2] and
+                                list(best.report.deactivated_per_round) == ref[3]) else "DIFFERENT"
+          print(f"{name:4s} {label:9s} pins {info.num_pins:11d} rounds {best.report.rounds:2d} |M| {len(ids):9d} "
+                f"device ms {best.report.device_ms:9.3f}  G pins/s {info.num_pins / best.report.device_ms / 1e6:7.2f}  {same}", flush=True)
+      dg.release()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["c1", "c2s", "c3s", "c4", "u8s"])
