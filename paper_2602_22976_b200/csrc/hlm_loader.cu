@@ -200,8 +200,9 @@ static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, ui
 int build_incidence(Graph* g) {
   if (g->voff) return HLM_B200_OK;
   ST_CHECK(dalloc(&g->voff, static_cast<size_t>(g->n) + 1));
-  ST_CHECK(dalloc(&g->vinc, g->kappa));
+  ST_CHECK(dalloc(&g->vinc, g->kappa + 4));  // one quad of padding: the CREW sweep loads 16 bytes at a time
   g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
+  CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 16, g->stream));
   return build_incidence_into(g, g->csr(), g->voff, g->vinc);
 }
 
