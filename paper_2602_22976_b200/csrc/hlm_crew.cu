@@ -61,7 +61,8 @@ struct CrewState {
   uint32_t* alive = nullptr;   // m bits, caller edge ids
   uint32_t* votes = nullptr;   // m 16-bit lanes: vertices whose argmax is this edge, this round
   uint32_t* vnew = nullptr;    // n bits: vertices covered in this round
-  uint8_t* gflag = nullptr;    // n/32: some list of this 32-vertex group may still be live
+  uint8_t* gflag = nullptr;    // n/32: 0 = no list of this 32-vertex group is live any more, else the group's class
+  uint8_t* gclass = nullptr;   // n/32: 1 = per-vertex offsets (voff), 2 = group-packed and staged through shared memory
   uint32_t* inv = nullptr;     // m: caller id -> resident row (null: same order)
   uint32_t num_heavy = 0, num_tasks = 0;
   uint32_t* heavy_v = nullptr;      // heavy vertex ids
@@ -281,6 +282,7 @@ void crew_release(Graph* g) {
   pool_free(c->votes);
   pool_free(c->vnew);
   pool_free(c->gflag);
+  pool_free(c->gclass);
   pool_free(c->inv);
   pool_free(c->heavy_v);
   pool_free(c->heavy_first);

@@ -51,6 +51,8 @@ def test_crew_matches_oracle(hb, port):
         g = port.generate_random(50 + 40 * seed, 80 + 70 * seed, 1 if seed % 4 == 0 else 2, 5, seed)
         if seed % 2 == 0:
             g.base_weights = port.random_weights_1_100(g.m, seed)
+        elif seed % 4 == 1:  # fractional weights: the caller's f64 array is read per incidence entry
+            g.base_weights = np.asarray(port.random_weights_1_100(g.m, seed), dtype=np.float64) * 0.37 + 0.11
         for s in _streams(seed * 3):
             want = port.local_max(g, s)
             got = hb.run_variant(to_hb_graph(g), to_hb_stream(s), hb.ParallelConfig(variant="crew"))
