@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/hlm_b200.h"
+#include "hlm_host_simd.h"
 #include "hlm_engine.h"
 #include "hlm_kernels.cuh"
 
@@ -463,19 +464,10 @@ struct HostScan {
       const uint64_t b = (is_off ? t - nc : t) * kChunk, e = std::min(m, b + kChunk);
       if (is_off) {
         if (nonuniform.load(std::memory_order_relaxed)) continue;
-        uint64_t bad = 0;
-        for (uint64_t i = b; i < e; ++i) bad |= (off[i + 1] - off[i]) ^ d0;
-        if (bad) nonuniform.store(true, std::memory_order_relaxed);
+        if (host_offsets_differ(off, d0, b, e)) nonuniform.store(true, std::memory_order_relaxed);
       } else {
         if (!nopack.load(std::memory_order_relaxed)) {
-          bool bad = false;
-          for (uint64_t i = b; i < e; ++i) {
-            const double x = w[i];
-            const uint32_t q = (x >= 1.0 && x <= 255.0) ? static_cast<uint32_t>(x) : 0u;
-            bad |= static_cast<double>(q) != x;
-            packed[i] = static_cast<uint8_t>(q);
-          }
-          if (bad) nopack.store(true, std::memory_order_relaxed);
+          if (host_pack_weights_u8(w, packed, b, e)) nopack.store(true, std::memory_order_relaxed);
         }
         weight_chunks_done.fetch_add(1, std::memory_order_release);
       }
