@@ -227,7 +227,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=os.environ.get("HLM_BENCH_WORKLOAD", "c2"))
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -341,7 +341,8 @@ def main():
     h2d = host.edge_offsets.nbytes + host.edge_members.nbytes + host.base_weights.nbytes
     dg.release()
     torch.cuda.synchronize()
-    hb.run_variant(host, stream, cfg, device=local_rank)  # warm
+    for _ in range(3):  # warm: the first calls still grow the memory pools (16-40 ms of device time instead of 9)
+        hb.run_variant(host, stream, cfg, device=local_rank)
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -350,7 +351,7 @@ def main():
     d2h = int(eres.matching.matched_edges.nbytes + eres.report.matched_round.nbytes + 8 * eres.report.rounds)
     assert np.array_equal(eres.matching.matched_edges, res.matching.matched_edges)
     e2e = {"value": kappa / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(eres.report.h2d_bytes),
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps, "warmup": 3,
            "host_input_bytes": int(h2d),
            "call": "hlm_b200_match_host (host scan/pack of offsets+weights || pin upload, loader kernels, matching, "
                    "result copy), pinned host CSR"}
