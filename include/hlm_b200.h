@@ -42,13 +42,20 @@ enum { HLM_B200_MODE_PERTURB_BASE = 0, HLM_B200_MODE_REPLACE_UNIFORM = 1 };
  * active lists every round, which is what work_optimal is for); their WorkCounters follow the
  * reference's own per-variant formulas.  GREEDY (greedy_sorted, local_max_seq.hpp:130) is the
  * lexicographically first maximal matching under (weight descending, id ascending): it runs on the
- * exact three-level path with that static order as the key and reports like the reference does. */
+ * exact three-level path with that static order as the key and reports like the reference does.
+ * AUTO (B200 extension, not in the reference's enum) is CRCW as far as the caller can tell -- the same
+ * matching, the same report, CRCW's WorkCounters -- with the engine chosen by the library: the
+ * vertex-owned CREW kernels when the per-vertex words of the instance outgrow L2 or its edges are
+ * ragged / long (there the atomics and the random filter-word reads of the CRCW kernels cost 1.7-3x),
+ * the CRCW kernels otherwise and always for the one-shot hlm_b200_match_host (the incidence side
+ * the CREW kernels need is built once per resident instance). */
 enum {
   HLM_B200_VARIANT_SEQ = 0,
   HLM_B200_VARIANT_CRCW = 1,
   HLM_B200_VARIANT_CREW = 2,
   HLM_B200_VARIANT_WORK_OPTIMAL = 3,
-  HLM_B200_VARIANT_GREEDY = 4
+  HLM_B200_VARIANT_GREEDY = 4,
+  HLM_B200_VARIANT_AUTO = 5
 };
 
 /* Borrowed view of hlm::Hypergraph (hypergraph.hpp:19-27): exactly its five arrays.  The vertex

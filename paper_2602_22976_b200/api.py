@@ -23,7 +23,8 @@ from . import _lib
 
 GENERATOR_KINDS = {"xorshift": 0, "park_miller": 1, "splitmix": 2}
 WEIGHT_MODES = {"perturb_base": 0, "replace_uniform": 1}
-VARIANTS = {"seq": 0, "crcw": 1, "crew": 2, "work_optimal": 3, "opt": 3, "greedy": 4}
+VARIANTS = {"seq": 0, "crcw": 1, "crew": 2, "work_optimal": 3, "opt": 3, "greedy": 4,
+            "auto": 5}  # auto: B200 extension -- crcw to the caller, engine chosen by the library
 LOOP_MODES = {"auto": 0, "host": 1, "graph": 2}
 TIE_MODES = {"auto": 0, "exact": 1}
 SYN_FAMILIES = {"uniform": 0, "rmat": 1, "powerlaw": 2, "netlist": 3}

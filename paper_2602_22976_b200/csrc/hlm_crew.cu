@@ -321,7 +321,8 @@ static int crew_setup(Graph* g) {
   return HLM_B200_OK;
 }
 
-static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out,
+                           int report_variant) {
   const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
   if (max_rounds > 65000u) {
     set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
@@ -402,18 +403,18 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
   }
   out->kernel_launches = launches;
   out->device_edge_visits = static_cast<uint64_t>(g->m) * round;
-  int rc = assemble_result(g, round, cfg, HLM_B200_VARIANT_CREW, out);
+  int rc = assemble_result(g, round, cfg, report_variant, out);
   if (rc != HLM_B200_OK) return rc;
   return limit ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
 
 #include "hlm_crew2.inc"
 
-int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
+int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out, int report_variant) {
   const char* env = std::getenv("HLM_B200_CREW_SOFT");
   // 16-bit vote lanes: an edge with more pins than that takes the soft-deletion form
-  if ((env && env[0] == '1') || g->max_edge_size > 65535u) return match_crew_soft(g, st, cfg, out);
-  return match_crew_compacting(g, st, cfg, out);
+  if ((env && env[0] == '1') || g->max_edge_size > 65535u) return match_crew_soft(g, st, cfg, out, report_variant);
+  return match_crew_compacting(g, st, cfg, out, report_variant);
 }
 
 }  // namespace hlmb

@@ -286,6 +286,7 @@ static int init_device(Graph* g, int device) {
   CU_CHECK(cudaSetDevice(device));
   g->device = device;
   CU_CHECK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CU_CHECK(cudaDeviceGetAttribute(&g->l2_bytes, cudaDevAttrL2CacheSize, device));
   CU_CHECK(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
   g->stream = g->own_stream;
   return HLM_B200_OK;
@@ -1349,6 +1350,28 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
     case HLM_B200_VARIANT_CREW:
       rc = match_crew(g, st, cfg, out);
       break;
+    case HLM_B200_VARIANT_AUTO: {
+      // CRCW wins where the edges are short and uniform and vtop (4 B per vertex) stays in L2
+      // (config 2: 6.2 vs 15.5 ms); the vertex-owned kernels win by 1.7-3x on ragged / long edges and
+      // once n * 4 B outgrows L2 (configs 3, 4, the config-5 shard shape).  HLM_B200_AUTO=crcw|crew.
+      // Measured (device ms, crcw / crew): RMAT graphs 2^26 edges 2.3 / 4.6, 2^28 edges 6.2 / 15.1;
+      // 4-uniform n = 1 M 0.45 / 0.49, n = 24 M 15.4 / 10.2, n = 32 M 15.1 / 8.8.
+      const uint64_t vtop_bytes = static_cast<uint64_t>(g->n) * 4, l2 = static_cast<uint64_t>(g->l2_bytes);
+      bool crcw = g->one_shot || g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
+                  (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4);
+      if (const char* env = std::getenv("HLM_B200_AUTO")) {
+        if (std::strcmp(env, "crew") == 0) crcw = false;
+        if (std::strcmp(env, "crcw") == 0) crcw = true;
+      }
+      if (crcw) {
+        hlm_b200_config as_crcw = *cfg;
+        as_crcw.variant = HLM_B200_VARIANT_CRCW;
+        rc = match_crcw(g, st, &as_crcw, out);
+      } else {
+        rc = match_crew(g, st, cfg, out, HLM_B200_VARIANT_CRCW);
+      }
+      break;
+    }
     case HLM_B200_VARIANT_GREEDY: {  // run_variant's greedy branch (local_max_par.hpp:597-612): no stream
       hlm_b200_stream none = {0, HLM_B200_GEN_XORSHIFT, HLM_B200_MODE_PERTURB_BASE, 0.0, 0.0};
       rc = match_crcw(g, &none, cfg, out);
@@ -1522,6 +1545,7 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   PhaseTrace tr;
   int rc = upload(host, device, &g, plan);
   if (rc != HLM_B200_OK) return rc;
+  g->one_shot = true;
   tr.mark("match_host: upload");
   // a single matching: building the CUDA graph (0.3 ms) costs more than the host loop's per-round
   // synchronisations save

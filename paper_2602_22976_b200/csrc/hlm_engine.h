@@ -66,6 +66,8 @@ struct CrewState;  // hlm_crew.cu
 struct Graph {
   int device = 0;
   int num_sms = 148;
+  int l2_bytes = 126 << 20;
+  bool one_shot = false;  // created by hlm_b200_match_host: lives for one matching
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   uint32_t n = 0, m = 0;
@@ -123,7 +125,9 @@ int build_base_codes(Graph* g);
 int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins);
 int generate(const hlm_b200_syn_spec* spec, int device, Graph** out);
 int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base);
-int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out);
+// report_variant: whose WorkCounters formulas the result carries (CREW, or CRCW when AUTO chose this engine)
+int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out,
+               int report_variant = HLM_B200_VARIANT_CREW);
 void crew_release(Graph* g);
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
                     hlm_b200_result* out, double weight_before = 0.0);

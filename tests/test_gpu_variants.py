@@ -112,3 +112,26 @@ def test_quality_band_vs_greedy_acceptance_criterion_7(hb, port):
         worst = min(worst, ratio)
     geomean = math.exp(logs / 100)
     assert geomean >= 0.85, (geomean, worst)
+
+
+def test_auto_is_crcw_to_the_caller_on_either_engine(hb, port, ref, monkeypatch):
+    """HLM_B200_VARIANT_AUTO (B200 extension): same matching, report and WorkCounters as crcw, whichever
+    engine the library picks (forced both ways here), on resident instances and through the one-shot
+    call (which always takes the CRCW kernels)."""
+    for name, g in _instances(port):
+        s = po.Stream(seed=9)
+        want = port.local_max(g, s)
+        theirs = ref.local_max(g, s, variant=po.VARIANT_CRCW, workers=2)
+        one_shot = hb.run_variant(to_hb_graph(g), to_hb_stream(s), hb.ParallelConfig(variant="auto"))
+        assert_same_result(one_shot, want, f"{name} auto one-shot")
+        dg = hb.DeviceHypergraph.upload(to_hb_graph(g))
+        for forced in (None, "crcw", "crew"):
+            if forced is None:
+                monkeypatch.delenv("HLM_B200_AUTO", raising=False)
+            else:
+                monkeypatch.setenv("HLM_B200_AUTO", forced)
+            got = dg.match(to_hb_stream(s), hb.ParallelConfig(variant="auto"))
+            assert_same_result(got, want, f"{name} auto forced={forced}")
+            assert got.report.work.total_edge_visits == theirs.edge_visits, f"{name} auto {forced}: edge visits"
+            assert got.report.work.total_pin_visits == theirs.pin_visits, f"{name} auto {forced}: pin visits"
+        dg.release()
