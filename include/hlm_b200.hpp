@@ -210,6 +210,17 @@ class ResidentHypergraph {
     return detail::finish(st, r);
   }
 
+  // B200 extension (HLM_B200_VARIANT_AUTO): Variant::crcw as far as the caller can tell -- the same
+  // matching, report and WorkCounters -- on whichever engine is faster for this instance.
+  MatchResult run_fastest(const WeightStream& stream, const ParallelConfig& cfg = ParallelConfig{}) const {
+    const hlm_b200_stream s = detail::stream_of(stream);
+    hlm_b200_config c = detail::config_of(cfg);
+    c.variant = HLM_B200_VARIANT_AUTO;
+    hlm_b200_result r;
+    const int st = hlm_b200_match(g_, &s, &c, &r);
+    return detail::finish(st, r);
+  }
+
   VerificationReport verify_matching(const Matching& m) const {
     int disjoint = 0, maximal = 0;
     double weight = 0.0;

@@ -49,6 +49,17 @@ int main() {
       CHECK(ver.valid());
       CHECK(ver.weight == verify_matching(h, got.matching).weight);
     }
+    {  // resident instance: upload once, match on the engine the library picks
+      const b200::ResidentHypergraph dev(h);
+      const MatchResult fast = dev.run_fastest(s);
+      ParallelConfig crcw;
+      crcw.variant = Variant::crcw;
+      const MatchResult plain = dev.run_variant(s, crcw);
+      CHECK(fast.matching.matched_edges == seq.matching.matched_edges);
+      CHECK(fast.report.matched_per_round == seq.report.matched_per_round);
+      CHECK(fast.report.work.total_pin_visits == plain.report.work.total_pin_visits);
+      CHECK(fast.report.work.total_edge_visits == plain.report.work.total_edge_visits);
+    }
     // every other entry point with the reference's signature
     {
       const MatchResult opt = b200::local_max_work_optimal(h, s);
