@@ -5,6 +5,9 @@
 //     hypergraph.hpp:144-151),
 //   * exclusive scan, download.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -154,22 +157,37 @@ int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out
 // ---------------------------------------------------------------------------------------------
 // vertex-incidence CSR (order inside one vertex's list is unspecified; no matcher depends on it)
 // ---------------------------------------------------------------------------------------------
-__global__ void k_degree(const uint32_t* pins, uint64_t kappa, uint32_t* deg) {
+// Both passes touch one word per pin at a random vertex.  Once the per-vertex array outgrows L2 those
+// are random HBM sectors (2 G of them cost ~300 ms on the 8-uniform shard shape), so the pins are
+// streamed several times instead, each time serving only the vertices of one window whose words
+// stay in L2: [vlo, vhi).
+__global__ void k_degree(const uint32_t* pins, uint64_t kappa, uint32_t vlo, uint32_t vhi, uint32_t* deg) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < kappa;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    atomicAdd(deg + pins[i], 1u);
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = __ldcs(pins + i);
+    if (v >= vlo && v < vhi) atomicAdd(deg + v, 1u);
+  }
 }
 
-__global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, const unsigned long long* voff,
-                                 uint32_t* cursor, const uint32_t* orig, uint32_t* vinc) {
+__global__ void k_copy_u64(const unsigned long long* in, uint64_t count, unsigned long long* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+// pos[v] starts as voff[v]; the returning 64-bit add hands out the slots of v's list
+__global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, uint32_t vhi, unsigned long long* pos,
+                                 const uint32_t* orig, uint32_t* vinc) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     uint64_t b;
     uint32_t s;
     csr.range(e, b, s);
-    const uint32_t id = orig ? orig[e] : e;  // incidence lists name edges by the caller's ids
+    uint32_t id = 0xffffffffu;  // incidence lists name edges by the caller's ids
     for (uint32_t i = 0; i < s; ++i) {
-      const uint32_t v = csr.pins[b + i];
-      vinc[voff[v] + atomicAdd(cursor + v, 1u)] = id;
+      const uint32_t v = __ldcs(csr.pins + b + i);
+      if (v < vlo || v >= vhi) continue;
+      if (id == 0xffffffffu) id = orig ? orig[e] : e;
+      vinc[atomicAdd(pos + v, 1ull)] = id;
     }
   }
 }
@@ -177,21 +195,47 @@ __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, const unsigned l
 // voff (n+1) / vinc (kappa) of the CSR `csr` over n vertices; edges are named by orig[] when given
 static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc) {
   cudaStream_t s = g->stream;
+  const bool trace = std::getenv("HLM_B200_TRACE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hlm_b200] incidence: %-20s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   uint32_t* deg = nullptr;
   ST_CHECK(dalloc(&deg, g->n));
   CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
-  if (g->kappa) k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(csr.pins, g->kappa, deg);
+  // window sizes: half of L2 for the words the atomics hit (4 B per vertex, then 8 B per vertex)
+  int l2 = 64 << 20;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+  uint64_t budget = std::max<uint64_t>(static_cast<uint64_t>(l2) / 2, 1u << 20);
+  if (const char* wenv = std::getenv("HLM_B200_INCIDENCE_WINDOW_MB")) budget = std::max<uint64_t>(1, std::strtoull(wenv, nullptr, 10)) << 20;
+  const uint32_t win4 = static_cast<uint32_t>(std::min<uint64_t>(0xffffffffu, budget / 4));
+  const uint32_t win8 = static_cast<uint32_t>(std::min<uint64_t>(0xffffffffu, budget / 8));
+  if (g->kappa)
+    for (uint64_t lo = 0; lo < g->n; lo += win4)
+      k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(csr.pins, g->kappa, static_cast<uint32_t>(lo),
+                                                      static_cast<uint32_t>(std::min<uint64_t>(g->n, lo + win4)), deg);
+  mark("degrees");
   int rc = device_exclusive_scan_u32_to_u64(g, deg, voff, g->n, nullptr);
-  if (rc != HLM_B200_OK) {
-    pool_free(deg);
-    return rc;
-  }
-  CU_CHECK(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
-  if (g->m)
-    k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(csr, g->m, reinterpret_cast<const unsigned long long*>(voff),
-                                                         deg, g->orig, vinc);
-  CU_CHECK(cudaStreamSynchronize(s));
   pool_free(deg);
+  if (rc != HLM_B200_OK) return rc;
+  mark("scan");
+  if (g->m && g->n) {
+    unsigned long long* pos = nullptr;
+    ST_CHECK(dalloc(&pos, g->n));
+    k_copy_u64<<<grid_of(g, g->n), kBlock, 0, s>>>(reinterpret_cast<const unsigned long long*>(voff), g->n, pos);
+    for (uint64_t lo = 0; lo < g->n; lo += win8)
+      k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(csr, g->m, static_cast<uint32_t>(lo),
+                                                           static_cast<uint32_t>(std::min<uint64_t>(g->n, lo + win8)), pos,
+                                                           g->orig, vinc);
+    CU_CHECK(cudaStreamSynchronize(s));
+    mark("fill");
+    pool_free(pos);
+  }
+  CU_CHECK(cudaStreamSynchronize(s));
   CU_CHECK(cudaGetLastError());
   return HLM_B200_OK;
 }
@@ -686,7 +730,14 @@ int renumber_by_degree(Graph* g) {
   g->device_bytes += static_cast<uint64_t>(g->n) * 4;
   CU_CHECK2(cudaMemsetAsync(deg, 0, static_cast<size_t>(g->n) * 4, s));
   CU_CHECK2(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb) * 4, s));
-  k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, deg);
+  {  // windows of vertices whose counters stay in L2 (see build_incidence_into)
+    int l2 = 64 << 20;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+    const uint32_t win = static_cast<uint32_t>(std::max(l2 / 2, 1 << 20) / 4);
+    for (uint64_t lo = 0; lo < g->n; lo += win)
+      k_degree<<<grid_of(g, g->kappa), kBlock, 0, s>>>(g->pins, g->kappa, static_cast<uint32_t>(lo),
+                                                      static_cast<uint32_t>(std::min<uint64_t>(g->n, lo + win)), deg);
+  }
   k_degree_hist<<<grid_of(g, g->n), kBlock, 0, s>>>(deg, g->n, hist);
   rc = device_exclusive_scan_u32_to_u64(g, hist, start, nb, nullptr);
   if (rc == HLM_B200_OK) {
