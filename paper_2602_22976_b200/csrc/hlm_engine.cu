@@ -353,10 +353,11 @@ int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins) {
 }
 
 // Weight constants: min / max of the base weights; drops the array when all are equal.
-int finish_weights(Graph* g) {
+int finish_weights(Graph* g, const WeightStats* known) {
   if (g->m == 0 || !g->base) return HLM_B200_OK;
   WeightStats ws;
-  ST_CHECK(weight_stats(g, 0.0, &ws));
+  if (known) ws = *known;
+  else ST_CHECK(weight_stats(g, 0.0, &ws));
   if (ws.non_positive) {
     set_error("an edge has a non-positive weight (hypergraph.hpp:104)");
     return HLM_B200_ERR_INPUT;
@@ -527,13 +528,48 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     for (unsigned t = 0; t + 1 < nt; ++t) workers.emplace_back([&scan] { scan.work([] {}); });
   }
   cudaError_t e = cudaSuccess;
-  if (g->kappa) e = cudaMemcpyAsync(g->pins, h->edge_members, g->kappa * 4, cudaMemcpyHostToDevice, s);
+  // The pins go up in 256 MB pieces; a second stream takes the largest vertex id of every piece
+  // while the next one is in flight, so the validation does not follow the last byte.
+  struct SideCheck {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev = nullptr;
+    EdgeStats* d_st = nullptr;
+    WeightStats* d_ws = nullptr;
+    ~SideCheck() {
+      if (s2) cudaStreamSynchronize(s2);
+      pool_free(d_st);
+      pool_free(d_ws);
+      if (ev) cudaEventDestroy(ev);
+      if (s2) cudaStreamDestroy(s2);
+    }
+  } side;
+  bool pins_checked = false;
+  const EdgeStats st_init = {0xffffffffu, 0, 0, 0, 0, 0};
+  if (g->kappa) {
+    if (assist && dev_alloc(&side.d_st, 1, nullptr) == HLM_B200_OK &&
+        cudaStreamCreateWithFlags(&side.s2, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&side.ev, cudaEventDisableTiming) == cudaSuccess) {
+      e = cudaMemcpyAsync(side.d_st, &st_init, sizeof(st_init), cudaMemcpyHostToDevice, side.s2);
+      const uint64_t piece = 64ull << 20;
+      for (uint64_t at = 0; at < g->kappa && e == cudaSuccess; at += piece) {
+        const uint64_t len = std::min(piece, g->kappa - at);
+        e = cudaMemcpyAsync(g->pins + at, h->edge_members + at, len * 4, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(side.ev, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(side.s2, side.ev, 0);
+        if (e == cudaSuccess) k_max_pin<<<grid_for(g, len), kBlock, 0, side.s2>>>(g->pins + at, len, side.d_st);
+      }
+      pins_checked = e == cudaSuccess;
+    } else {
+      cudaGetLastError();
+      e = cudaMemcpyAsync(g->pins, h->edge_members, g->kappa * 4, cudaMemcpyHostToDevice, s);
+    }
+  }
   g->h2d_bytes = g->kappa * 4;
   tr.mark("upload: pins copy queued");
 
   // ---- weights: queued behind the pins as soon as the host has looked at all of them
   uint8_t* d_codes = nullptr;
-  bool weights_queued = false;
+  bool weights_queued = false, code_stats_queued = false;
   auto queue_weights = [&]() {
     if (weights_queued || !m || e != cudaSuccess || rc != HLM_B200_OK) return;
     if (assist && !scan.weights_ready()) return;
@@ -542,6 +578,14 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
       if ((rc = dev_alloc(&d_codes, m, nullptr)) != HLM_B200_OK) return;
       e = cudaMemcpyAsync(d_codes, scan.packed, m, cudaMemcpyHostToDevice, s);
       k_expand_u8<<<grid_for(g, m), kBlock, 0, s>>>(d_codes, m, g->base);
+      // the weight statistics from the codes (1 byte instead of 8 per edge), still inside the upload
+      if (dev_alloc(&side.d_ws, 1, nullptr) == HLM_B200_OK) {
+        static const WeightStats ws_init = {~0ull, 0ull, 0u, 0u};
+        if (cudaMemcpyAsync(side.d_ws, &ws_init, sizeof(ws_init), cudaMemcpyHostToDevice, s) == cudaSuccess) {
+          k_code_stats<<<grid_for(g, m), kBlock, 0, s>>>(d_codes, m, side.d_ws);
+          code_stats_queued = true;
+        }
+      }
       g->h2d_bytes += m;
     } else {
       e = cudaMemcpyAsync(g->base, h->base_weights, static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, s);
@@ -555,6 +599,9 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   }
   queue_weights();
   tr.mark("upload: host scan + pack");
+  WeightStats code_ws = {~0ull, 0ull, 0u, 0u};
+  if (e == cudaSuccess && rc == HLM_B200_OK && code_stats_queued)
+    e = cudaMemcpyAsync(&code_ws, side.d_ws, sizeof(code_ws), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && rc == HLM_B200_OK) e = cudaStreamSynchronize(s);
   pool_free(d_codes);
   if (scan.packed) host_result_free(scan.packed);
@@ -573,7 +620,19 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     g->uniform_d = static_cast<uint32_t>(scan.d0);
     g->max_edge_size = g->uniform_d;
     g->num_large = 0;
-    if (g->kappa) {
+    if (g->kappa && pins_checked) {
+      EdgeStats st = st_init;
+      e = cudaMemcpyAsync(&st, side.d_st, sizeof(st), cudaMemcpyDeviceToHost, side.s2);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(side.s2);
+      if (e != cudaSuccess) {
+        set_error("pin validation failed: %s", cudaGetErrorString(e));
+        return fail(HLM_B200_ERR_CUDA);
+      }
+      if (st.max_pin >= g->n) {
+        set_error("vertex id %u out of range [0, %u)", st.max_pin, g->n);
+        return fail(HLM_B200_ERR_INPUT);
+      }
+    } else if (g->kappa) {
       EdgeStats* d_st = nullptr;
       if ((rc = dev_alloc(&d_st, 1, nullptr)) != HLM_B200_OK) return fail(rc);
       EdgeStats st = {0xffffffffu, 0, 0, 0, 0, 0};
@@ -606,7 +665,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     if ((rc = finish_graph(g, off64, true)) != HLM_B200_OK) return fail(rc);
   }
   tr.mark("upload: edge structure");
-  if ((rc = finish_weights(g)) != HLM_B200_OK) return fail(rc);
+  if ((rc = finish_weights(g, code_stats_queued ? &code_ws : nullptr)) != HLM_B200_OK) return fail(rc);
   tr.mark("upload: weight stats");
   if (plan.reorder && reorder_enabled() && renumber_enabled() && (rc = renumber_by_degree(g)) != HLM_B200_OK) return fail(rc);
   if (plan.reorder && reorder_enabled() && (rc = reorder_by_first_pin(g)) != HLM_B200_OK) return fail(rc);

@@ -113,7 +113,9 @@ void host_result_free(void* p);
 uint32_t default_max_rounds(uint32_t m);
 int new_graph(int device, Graph** out);
 int finish_graph(Graph* g, uint64_t* off64_dev, bool check_pins);
-int finish_weights(Graph* g);
+struct WeightStats;
+// known: statistics the loader already has (from the packed byte codes); null = one pass over g->base
+int finish_weights(Graph* g, const WeightStats* known = nullptr);
 int weight_stats(Graph* g, double lo, WeightStats* out);
 int build_incidence(Graph* g);
 int ensure_workspace(Graph* g, uint32_t max_rounds);

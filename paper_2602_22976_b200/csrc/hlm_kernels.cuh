@@ -1150,6 +1150,24 @@ __global__ void k_max_pin(const uint32_t* pins, uint64_t kappa, EdgeStats* st) {
   if ((threadIdx.x & 31) == 0) atomicMax(&st->max_pin, mx);
 }
 
+// the statistics k_weight_stats takes from the f64 weights, from the byte codes the host packed
+// (integers 0..255, lo = 0): 1/8 of the bytes
+__global__ void k_code_stats(const uint8_t* __restrict__ codes, uint32_t m, WeightStats* st) {
+  uint32_t mn = 255u, mx = 0u;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint32_t c = codes[e];
+    mn = min(mn, c);
+    mx = max(mx, c);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&st->min_bits, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(mn))));
+    atomicMax(&st->max_bits, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(mx))));
+    if (mn == 0u) atomicOr(&st->non_positive, 1u);
+  }
+}
+
 __global__ void k_narrow_offsets(const uint64_t* off64, uint32_t* off32, uint64_t count) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
