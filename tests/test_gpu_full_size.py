@@ -47,6 +47,15 @@ def test_full_size_matching_equals_the_reference(hb, ref, name, spec):
     again = dg.match(s, hb.ParallelConfig(variant="crcw", loop_mode="host"))
     assert np.array_equal(again.matching.matched_edges, got.matching.matched_edges)
     assert again.report.matched_per_round_count == got.report.matched_per_round_count
+    # the vertex-owned CREW kernels (staged groups, tasks of hub vertices, fire-and-forget kill) and the
+    # engine `auto` picks must give the same matching and the same per-round report at full size
+    for variant in ("crew", "auto"):
+        other = dg.match(s, hb.ParallelConfig(variant=variant))
+        assert np.array_equal(other.matching.matched_edges, got.matching.matched_edges), variant
+        assert other.report.matched_per_round_count == got.report.matched_per_round_count, variant
+        assert other.report.deactivated_per_round == got.report.deactivated_per_round, variant
+        assert other.matching.total_weight == got.matching.total_weight, variant
+        assert np.array_equal(other.report.matched_round, got.report.matched_round), variant
     # the reference itself on the same instance
     need_gib = (info.num_pins * 8 + info.num_edges * 24 + info.num_vertices * 8) * 2.2 / (1 << 30)
     if _host_gib() < need_gib + 8:
