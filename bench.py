@@ -341,16 +341,17 @@ def main():
     h2d = host.edge_offsets.nbytes + host.edge_members.nbytes + host.base_weights.nbytes
     dg.release()
     torch.cuda.synchronize()
+    e2e_cfg = hb.ParallelConfig(variant="crcw")  # the call a user makes: default loop mode (host loop for one matching)
     for _ in range(3):  # warm: the first calls still grow the memory pools (16-40 ms of device time instead of 9);
         # the result stays bound like in the timed loop, so the second set of page-locked result arrays
         # (the previous result is still alive when the next call returns) is allocated here, not there
-        eres = hb.run_variant(host, stream, cfg, device=local_rank)
+        eres = hb.run_variant(host, stream, e2e_cfg, device=local_rank)
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
     t0 = time.perf_counter()
     e2e_each = []
     for _ in range(e2e_steps):
         t1 = time.perf_counter()
-        eres = hb.run_variant(host, stream, cfg, device=local_rank)
+        eres = hb.run_variant(host, stream, e2e_cfg, device=local_rank)
         e2e_each.append(round((time.perf_counter() - t1) * 1e3, 2))
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     d2h = int(eres.matching.matched_edges.nbytes + eres.report.matched_round.nbytes + 8 * eres.report.rounds)
