@@ -156,6 +156,16 @@ def reference_arm(args, wl):
     kind = "reference" if po.reference_available() else "port"
     orc = po.Oracle(kind)
     gen = po.Oracle("port")
+    if args.gpus > 1:
+        # the N > 1 arm of this repo runs the config-5 shape (multi_gpu.bench_main): the same here,
+        # 1/128 of it (the whole instance does not fit host memory, nor a few minutes of CPU time)
+        per_m = int(os.environ.get("HLM_BENCH_MG_EDGES", 250_000_000))
+        per_n = int(os.environ.get("HLM_BENCH_MG_VERTICES", 125_000_000))
+        n5, m5 = per_n * args.gpus, per_m * args.gpus
+        wl = dict(desc=f"config 5 shape: 8-uniform, n={n5}, m={m5} edge-partitioned over {args.gpus} GPUs "
+                       f"({per_m} edges per GPU), unit weights, default stream",
+                  sample=dict(family="uniform", n=max(1000, n5 // 128), m=max(1000, m5 // 128), d=8, seed=1, int_weights=False),
+                  sample_desc="same generator at 1/128 of the vertices and edges")
     s = wl["sample"]
     fam = {"uniform": po.SYN_UNIFORM, "rmat": po.SYN_RMAT, "powerlaw": po.SYN_POWERLAW, "netlist": po.SYN_NETLIST}[s["family"]]
     g = gen.syn_generate(fam, n=s.get("n", 0), m=s["m"], d=s.get("d", 0), scale=s.get("scale", 0), seed=s["seed"],
