@@ -89,7 +89,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def begin(self):
+        """The timed region starts here (nvidia-smi was started earlier: it needs ~0.2 s to come up)."""
+        self.t_begin = time.time()
 
     def stop(self) -> dict:
         if not self.proc:
@@ -101,7 +105,11 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
-        for ln in self.lines:
+        t_begin = getattr(self, "t_begin", 0.0)
+        window = [ln for t, ln in self.lines if t >= t_begin]
+        if len(window) < 3:  # a very short region: the samples around it
+            window = [ln for t, ln in self.lines if t >= t_begin - 0.2]
+        for ln in window:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 8:
                 continue
@@ -264,6 +272,15 @@ def main():
     if sharded:
         import torch.distributed as dist_mod
 
+        # NCCL writes its version line to stdout: everything but the one JSON line goes to stderr
+        sys.stdout.flush()
+        json_fd = os.dup(1)
+        os.dup2(2, 1)
+
+        def emit(text):
+            sys.stdout.flush()
+            os.write(json_fd, (text + "\n").encode())
+
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
         os.environ.setdefault("RANK", "0")
@@ -274,7 +291,7 @@ def main():
 
         hbm_gbs, peak_src = load_peaks()
         multi_gpu.bench_main(args, wl, rank, world, local_rank, dist,
-                             extras=dict(sampler=ClockSampler(local_rank) if rank == 0 else None,
+                             extras=dict(emit=emit, sampler=ClockSampler(local_rank) if rank == 0 else None,
                                          algorithmic_bytes=algorithmic_bytes, hbm_gbs=hbm_gbs, peak_src=peak_src))
         dist_mod.destroy_process_group()
         return
@@ -292,11 +309,12 @@ def main():
     torch.cuda.set_stream(tstream)
     dg.set_stream(tstream.cuda_stream)
 
+    sampler = ClockSampler(local_rank)
+    sampler.start()  # before the warm-up: nvidia-smi needs a moment before its first line
     for _ in range(max(3, args.warmup)):
         res = dg.match(stream, cfg)
-    sampler = ClockSampler(local_rank)
-    sampler.start()
     torch.cuda.synchronize()
+    sampler.begin()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     dev_ms = []

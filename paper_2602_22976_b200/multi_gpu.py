@@ -395,13 +395,15 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
     stream = WeightStream()
     cfg = ParallelConfig(variant="crcw")
     extras = extras or {}
-    for _ in range(max(3, args.warmup)):
-        res = sm.match(stream, cfg, gather=False)
     sampler = extras.get("sampler")
     if sampler:
-        sampler.start()
+        sampler.start()  # before the warm-up: nvidia-smi needs a moment before its first line
+    for _ in range(max(3, args.warmup)):
+        res = sm.match(stream, cfg, gather=False)
     dist.barrier()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.begin()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(eng.stream):
         ev0.record(eng.stream)
@@ -445,5 +447,6 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
                                            "fit host memory)"},
                 "e2e": {"value": value, "unit": "pins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "note": "instance generated on the devices (16 G pins do not fit host memory)"}}
-        print(json.dumps(line), flush=True)
+        emit = extras.get("emit") or (lambda text: print(text, flush=True))
+        emit(json.dumps(line))
     dist.barrier()
