@@ -550,7 +550,8 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
         cudaStreamCreateWithFlags(&side.s2, cudaStreamNonBlocking) == cudaSuccess &&
         cudaEventCreateWithFlags(&side.ev, cudaEventDisableTiming) == cudaSuccess) {
       e = cudaMemcpyAsync(side.d_st, &st_init, sizeof(st_init), cudaMemcpyHostToDevice, side.s2);
-      const uint64_t piece = 64ull << 20;
+      uint64_t piece = 64ull << 20;  // entries: 256 MB
+      if (const char* penv = std::getenv("HLM_B200_PIN_PIECE_MB")) piece = std::max<uint64_t>(1, std::strtoull(penv, nullptr, 10)) << 18;
       for (uint64_t at = 0; at < g->kappa && e == cudaSuccess; at += piece) {
         const uint64_t len = std::min(piece, g->kappa - at);
         e = cudaMemcpyAsync(g->pins + at, h->edge_members + at, len * 4, cudaMemcpyHostToDevice, s);
