@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HLM_B200_ABI_VERSION 2
+#define HLM_B200_ABI_VERSION 3
 
 typedef enum {
   HLM_B200_OK = 0,
@@ -29,7 +29,8 @@ typedef enum {
   HLM_B200_ERR_ROUND_LIMIT = 2, /* hlm::round_limit_error (matching.hpp:77); partial result filled */
   HLM_B200_ERR_CUDA = 3,        /* CUDA runtime failure / no device */
   HLM_B200_ERR_NOMEM = 4,
-  HLM_B200_ERR_UNSUPPORTED = 5  /* e.g. a Variant this library does not implement */
+  HLM_B200_ERR_UNSUPPORTED = 5, /* e.g. a Variant this library does not implement */
+  HLM_B200_ERR_NCCL = 6         /* libnccl.so.2 missing, or a collective failed */
 } hlm_b200_status;
 
 /* hlm::GeneratorKind / hlm::WeightMode (weight_stream.hpp:17-22), same enumerator order. */
@@ -91,6 +92,11 @@ typedef struct {
   int32_t tie_mode;     /* HLM_B200_TIES_AUTO: 64-bit keys + detection + exact redo of a tied round;
                            HLM_B200_TIES_EXACT: three-level (w, tie_hash, id) keys every round */
   uint32_t flags;       /* HLM_B200_FLAG_* */
+  uint32_t num_gpus;    /* hlm_b200_match_host only: 0 / 1 = one device; k > 1 = the edge rows are cut into k
+                           blocks, block i goes to device (first + i) mod hlm_b200_device_count(), and the
+                           blocks are matched as one instance by hlm_b200_match_sharded (blocks that share a
+                           device run as co-located shards).  The result does not depend on k -- the
+                           reference's "independent of workers" (tests/test_par.cpp:32-55). */
 } hlm_b200_config;
 
 #define HLM_B200_FLAG_NO_ROUND_OF 1u   /* do not return matched_round */
@@ -165,6 +171,9 @@ int hlm_b200_device_count(void);
  * (tools/hlm_app.hpp:156-165).  Narrows offsets, detects uniform edge size / unit weights, bins
  * large edges, uploads to HBM.  The host arrays are not retained. */
 int hlm_b200_graph_upload(const hlm_b200_csr_view* host, int device, hlm_b200_graph** out);
+/* The same for one shard of an edge-partitioned instance: `rows` holds the edges [edge_begin, edge_begin +
+ * rows->num_edges) of the instance (offsets rebased to 0, vertex ids global); see hlm_b200_match_sharded. */
+int hlm_b200_graph_upload_shard(const hlm_b200_csr_view* rows, uint32_t edge_begin, int device, hlm_b200_graph** out);
 int hlm_b200_graph_generate(const hlm_b200_syn_spec* spec, int device, hlm_b200_graph** out);
 int hlm_b200_graph_info_get(const hlm_b200_graph* g, hlm_b200_graph_info* info);
 /* Copies the instance back into caller-allocated host arrays (any pointer may be NULL);
@@ -194,44 +203,47 @@ int hlm_b200_verify(hlm_b200_graph* g, const uint32_t* matched, uint64_t count, 
 int hlm_b200_eval_stream(const hlm_b200_stream* stream, const uint32_t* edges, const uint32_t* rounds,
                          const double* base, size_t count, double* w_out, uint64_t* t_out, int device);
 
-/* ---- edge-partitioned (multi-GPU) runs -----------------------------------------------------
- * No reference counterpart (the reference is single-process; PAPER.md:418 only sketches it).
- * One process per GPU holds the edge rows [edge_begin, edge_begin + m_local) of the instance
- * (hlm_b200_syn_spec, or an uploaded shard) and the replicated per-vertex arrays.  The caller
- * owns the two device arrays that cross ranks and all-reduces them between the steps
- * (paper_2602_22976_b200/multi_gpu.py does it with torch.distributed / NCCL); the protocol is
- * documented at the top of csrc/hlm_multi.inc.  Results are identical for every rank count. */
-typedef struct {
-  double base_min;      /* of the local base weights */
-  double base_max;
-  int32_t non_integer;  /* some fl(base + noise_low) is not an integer below 2^32 */
-  uint32_t num_edges;
-} hlm_b200_weight_info;
+/* ---- edge-partitioned (multi-GPU) runs: round driver in C++, collectives by NCCL --------------
+ * No reference counterpart (the reference is single-process; PAPER.md:418 only sketches it).  The round loop, the collectives and the tie handling
+ * all live behind one call; the host waits for the device once per round (a 32-byte read-back).
+ * Every shard holds the edge rows [edge_begin, edge_begin + m_local) of the instance and the
+ * incidence lists of its own edges; per round the ranks all-reduce(max) one uint64 per LIVE vertex
+ * and all-reduce(sum) the covered-vertex bitmap (csrc/hlm_shard.inc has the protocol).
+ *
+ * hlm_b200_comm: one rank of an NCCL communicator (one process per GPU).  Rank 0 calls
+ * hlm_b200_comm_unique_id and ships the 128 bytes to the other ranks by any means (bench.py:
+ * torch.distributed broadcast); every rank then calls hlm_b200_comm_create.  libnccl.so.2 is bound
+ * at run time (the copy already loaded in the process, if any). */
+#define HLM_B200_UNIQUE_ID_BYTES 128
+typedef struct hlm_b200_comm hlm_b200_comm;
+int hlm_b200_comm_unique_id(uint8_t* id /* HLM_B200_UNIQUE_ID_BYTES */);
+int hlm_b200_comm_create(const uint8_t* id, int rank, int nranks, int device, hlm_b200_comm** out);
+int hlm_b200_comm_info(const hlm_b200_comm* comm, int* rank, int* nranks, int* device, int* nccl_version);
+void hlm_b200_comm_destroy(hlm_b200_comm* comm);
 
 typedef struct {
-  void* vkey;                 /* device, uint64[num_vertices]: all-reduce(max) as int64 */
-  void* exch;                 /* device, int32[hlm_b200_mg_exch_words(n)]: all-reduce(sum) */
-  double base_min;            /* GLOBAL weight facts (reduce hlm_b200_graph_weight_info over ranks) */
-  double base_max;
-  int32_t non_integer;
-  uint32_t num_edges_global;  /* for default_max_rounds */
-} hlm_b200_mg_setup;
+  uint32_t rounds;
+  uint32_t num_local_shards;
+  uint32_t num_processes;
+  uint32_t tie_redo_rounds;  /* rounds resolved by the three-level comparator across ranks */
+  uint32_t host_syncs;       /* stream synchronisations inside the round loop: rounds + tie_redo_rounds */
+  uint32_t kernel_launches;
+  uint32_t nccl_calls;
+  uint64_t num_edges_global;
+  uint64_t collective_bytes;             /* payload handed to the collectives by one rank, all rounds */
+  uint64_t* collective_bytes_per_round;  /* rounds entries: shrinks with the live-vertex set */
+  uint32_t* live_vertices_per_round;     /* rounds entries: vertices whose maxima were exchanged */
+} hlm_b200_shard_report;
 
-enum { HLM_B200_MG_RUNNING = 0, HLM_B200_MG_DONE = 1, HLM_B200_MG_ROUND_LIMIT = 2 };
-
-uint64_t hlm_b200_mg_exch_words(uint32_t num_vertices);
-int hlm_b200_graph_weight_info(hlm_b200_graph* g, double noise_low, hlm_b200_weight_info* info);
-int hlm_b200_mg_begin(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
-                      const hlm_b200_mg_setup* setup);
-int hlm_b200_mg_vertex_max(hlm_b200_graph* g);
-int hlm_b200_mg_claims(hlm_b200_graph* g);
-int hlm_b200_mg_decide(hlm_b200_graph* g, uint32_t* global_active, int* tie);
-int hlm_b200_mg_check_commit(hlm_b200_graph* g);
-int hlm_b200_mg_exact_level(hlm_b200_graph* g, int level, void* va, void* vb, void* vc);
-int hlm_b200_mg_end_round(hlm_b200_graph* g, uint32_t global_active, int* status);
-/* weight_before: total_weight of the shards with lower edge ids (the reference sums base weights
- * in ascending-id order, local_max_seq.hpp:79; FP64 addition is not associative). */
-int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result* out);
+/* run_variant (local_max_par.hpp:586) over the shards `shards[0 .. num_shards)` of this process (ascending
+ * edge-id ranges; shards on one device are co-located "virtual ranks") and, if `comm` is given, the shards
+ * of the other processes.  results[i] receives shard i's slice (global edge ids, ascending) together with
+ * the GLOBAL rounds, per-round counts and total_weight; concatenating the slices in rank order gives the
+ * reference's matched_edges.  HLM_B200_TIES_EXACT in cfg resolves every round by the three-level comparator. */
+int hlm_b200_match_sharded(hlm_b200_graph* const* shards, int num_shards, hlm_b200_comm* comm,
+                           const hlm_b200_stream* stream, const hlm_b200_config* cfg, hlm_b200_result* results,
+                           hlm_b200_shard_report* report);
+void hlm_b200_shard_report_free(hlm_b200_shard_report* report);
 
 /* ---- text formats (host only, no device needed) ------------------------------------------------
  * io.hpp of the reference: hMetis .hgr hypergraphs (parse_hgr :79, write_hgr :146), METIS graphs

@@ -66,6 +66,7 @@ inline hlm_b200_config config_of(const ParallelConfig& cfg) {
   c.loop_mode = HLM_B200_LOOP_AUTO;
   c.tie_mode = HLM_B200_TIES_AUTO;
   c.flags = 0;
+  c.num_gpus = 0;
   return c;
 }
 
@@ -112,11 +113,14 @@ inline MatchResult finish(int status, hlm_b200_result& r) {
 }  // namespace detail
 
 // run_variant (local_max_par.hpp:586): upload + match + release in one synchronous call.
+// num_gpus > 1 (B200 extension): the edge rows are cut into that many blocks over the visible devices
+// (hlm_b200_config::num_gpus); the result is the same for every value.
 inline MatchResult run_variant(const Hypergraph& h, const WeightStream& stream, const ParallelConfig& cfg,
-                               int device = 0) {
+                               int device = 0, unsigned num_gpus = 0) {
   const hlm_b200_csr_view v = detail::view_of(h);
   const hlm_b200_stream s = detail::stream_of(stream);
-  const hlm_b200_config c = detail::config_of(cfg);
+  hlm_b200_config c = detail::config_of(cfg);
+  c.num_gpus = num_gpus;
   hlm_b200_result r;
   const int st = hlm_b200_match_host(&v, &s, &c, device, &r);
   return detail::finish(st, r);

@@ -7,7 +7,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HLM_B200_LIB") or os.path.join(_HERE, "lib", "libhlm_b200.so")
 
-OK, ERR_INPUT, ERR_ROUND_LIMIT, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = range(6)
+OK, ERR_INPUT, ERR_ROUND_LIMIT, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED, ERR_NCCL = range(7)
+UNIQUE_ID_BYTES = 128
 
 
 class CsrView(C.Structure):
@@ -24,7 +25,7 @@ class Stream(C.Structure):
 
 class Config(C.Structure):
     _fields_ = [("variant", C.c_int32), ("max_rounds", C.c_uint32), ("loop_mode", C.c_int32),
-                ("tie_mode", C.c_int32), ("flags", C.c_uint32)]
+                ("tie_mode", C.c_int32), ("flags", C.c_uint32), ("num_gpus", C.c_uint32)]
 
 
 class Result(C.Structure):
@@ -54,14 +55,12 @@ class SynSpec(C.Structure):
                 ("edge_begin", C.c_uint32), ("m_local", C.c_uint32)]
 
 
-class WeightInfo(C.Structure):
-    _fields_ = [("base_min", C.c_double), ("base_max", C.c_double), ("non_integer", C.c_int32),
-                ("num_edges", C.c_uint32)]
-
-
-class MgSetup(C.Structure):
-    _fields_ = [("vkey", C.c_void_p), ("exch", C.c_void_p), ("base_min", C.c_double), ("base_max", C.c_double),
-                ("non_integer", C.c_int32), ("num_edges_global", C.c_uint32)]
+class ShardReport(C.Structure):
+    _fields_ = [("rounds", C.c_uint32), ("num_local_shards", C.c_uint32), ("num_processes", C.c_uint32),
+                ("tie_redo_rounds", C.c_uint32), ("host_syncs", C.c_uint32), ("kernel_launches", C.c_uint32),
+                ("nccl_calls", C.c_uint32), ("num_edges_global", C.c_uint64), ("collective_bytes", C.c_uint64),
+                ("collective_bytes_per_round", C.POINTER(C.c_uint64)),
+                ("live_vertices_per_round", C.POINTER(C.c_uint32))]
 
 
 class HostGraph(C.Structure):
@@ -82,6 +81,7 @@ SYMBOLS = {
     "hlm_b200_last_error": (C.c_char_p, []),
     "hlm_b200_device_count": (C.c_int, []),
     "hlm_b200_graph_upload": (C.c_int, [C.POINTER(CsrView), C.c_int, C.POINTER(C.c_void_p)]),
+    "hlm_b200_graph_upload_shard": (C.c_int, [C.POINTER(CsrView), C.c_uint32, C.c_int, C.POINTER(C.c_void_p)]),
     "hlm_b200_graph_generate": (C.c_int, [C.POINTER(SynSpec), C.c_int, C.POINTER(C.c_void_p)]),
     "hlm_b200_graph_info_get": (C.c_int, [C.c_void_p, C.POINTER(GraphInfo)]),
     "hlm_b200_graph_download": (C.c_int, [C.c_void_p] * 6),
@@ -96,16 +96,14 @@ SYMBOLS = {
     "hlm_b200_eval_stream": (C.c_int, [C.POINTER(Stream), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                        C.c_void_p, C.c_void_p, C.c_int]),
     "hlm_b200_default_max_rounds": (C.c_uint32, [C.c_uint32]),
-    "hlm_b200_mg_exch_words": (C.c_uint64, [C.c_uint32]),
-    "hlm_b200_graph_weight_info": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(WeightInfo)]),
-    "hlm_b200_mg_begin": (C.c_int, [C.c_void_p, C.POINTER(Stream), C.POINTER(Config), C.POINTER(MgSetup)]),
-    "hlm_b200_mg_vertex_max": (C.c_int, [C.c_void_p]),
-    "hlm_b200_mg_claims": (C.c_int, [C.c_void_p]),
-    "hlm_b200_mg_decide": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
-    "hlm_b200_mg_check_commit": (C.c_int, [C.c_void_p]),
-    "hlm_b200_mg_exact_level": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
-    "hlm_b200_mg_end_round": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_int)]),
-    "hlm_b200_mg_finish": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(Result)]),
+    "hlm_b200_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "hlm_b200_comm_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "hlm_b200_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]),
+    "hlm_b200_comm_destroy": (None, [C.c_void_p]),
+    "hlm_b200_match_sharded": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.POINTER(Stream),
+                                         C.POINTER(Config), C.POINTER(Result), C.POINTER(ShardReport)]),
+    "hlm_b200_shard_report_free": (None, [C.POINTER(ShardReport)]),
     "hlm_b200_parse_hgr": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
     "hlm_b200_parse_metis_graph": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
     "hlm_b200_host_graph_free": (None, [C.POINTER(HostGraph)]),

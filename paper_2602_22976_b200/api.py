@@ -86,6 +86,7 @@ class ParallelConfig:
     tie_mode: str = "auto"    # B200 extension: "exact" forces the three-level comparator
     want_round_of: bool = True
     kernel_times: bool = False  # B200 extension (host loop): CUDA-event time of each round kernel
+    num_gpus: int = 0         # B200 extension (run_variant with host arrays): edge blocks over k devices
 
     def _c(self) -> _lib.Config:
         if isinstance(self.variant, str):
@@ -95,7 +96,8 @@ class ParallelConfig:
         else:
             variant = int(self.variant)
         flags = (0 if self.want_round_of else 1) | (2 if self.kernel_times else 0)
-        return _lib.Config(variant, self.max_rounds, LOOP_MODES[self.loop_mode], TIE_MODES[self.tie_mode], flags)
+        return _lib.Config(variant, self.max_rounds, LOOP_MODES[self.loop_mode], TIE_MODES[self.tie_mode], flags,
+                           int(self.num_gpus))
 
 
 @dataclass
@@ -167,7 +169,7 @@ def _raise(status: int, what: str):
         raise NotImplementedError(msg)
     if status == _lib.ERR_NOMEM:
         raise MemoryError(msg)
-    raise DeviceError(msg)
+    raise DeviceError(msg)  # ERR_CUDA, ERR_NCCL
 
 
 def _take(ptr, count, dtype):

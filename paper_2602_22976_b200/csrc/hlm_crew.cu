@@ -17,11 +17,13 @@
 // exact: ties are resolved inline, so there is no tie flag and no exact redo here.
 // Per-edge state is indexed by the caller's edge ids (the incidence lists name edges that way).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
 
+#include "hlm_comm.h"
 #include "hlm_engine.h"
 
 namespace hlmb {
@@ -47,7 +49,7 @@ constexpr uint32_t kMidDeg = 2048;
 struct CrewState {
   unsigned long long* wkey = nullptr;  // m: weight bits of active edges, 0 otherwise
   uint8_t* estat = nullptr;            // m: EdgeStatus (matching.hpp:50)
-  uint32_t* top = nullptr;             // n: T[v]
+  uint32_t* top = nullptr;             // n: T[v] (work-optimal form: the raw incidence entry, id | first-pin flag)
   uint8_t* vdead = nullptr;            // n
   uint32_t* vlist[3] = {nullptr, nullptr, nullptr};  // light / mid / hub vertex ids
   uint32_t vcount[3] = {0, 0, 0};
@@ -59,7 +61,6 @@ struct CrewState {
   uint8_t* ww8 = nullptr;      // kappa: the same, moving with winc
   uint32_t* vlen = nullptr;    // n: live length of a light vertex's list (0: heavy, dead or isolated)
   uint32_t* alive = nullptr;   // m bits, caller edge ids
-  uint32_t* votes = nullptr;   // m 16-bit lanes: vertices whose argmax is this edge, this round
   uint32_t* vnew = nullptr;    // n bits: vertices covered in this round
   uint8_t* gflag = nullptr;    // n/32: 0 = no list of this 32-vertex group is live any more, else the group's class
   uint8_t* gclass = nullptr;   // n/32: 1 = per-vertex offsets (voff), 2 = group-packed and staged through shared memory
@@ -74,6 +75,9 @@ struct CrewState {
   uint32_t* task_len = nullptr;     // live length
   unsigned long long* part_key = nullptr;  // per task: best key of the chunk
   uint32_t* part_id = nullptr;
+  // ---- edge-partitioned runs (hlm_shard.inc) ----
+  unsigned long long* lkey = nullptr;  // n: this shard's maximum at every live vertex (live-slot order)
+  uint32_t* mnow = nullptr;            // m bits: matched in the round in progress, not yet committed
 };
 
 struct CrewParams {
@@ -92,6 +96,7 @@ struct CrewParams {
   uint32_t* mbits;
   uint16_t* mround;
   uint32_t* counters;
+  uint32_t id_mask;  // incidence entries carry a first-pin flag in bit 31 when the instance has < 2^31 edges
 };
 
 template <typename T>
@@ -150,7 +155,7 @@ __global__ void k_crew_argmax_light(const CrewParams P, const uint32_t* list, ui
     unsigned long long bk = 0;
     uint32_t bid = kNoEdge;
     for (unsigned long long p = P.voff[v]; p < P.voff[v + 1]; ++p) {
-      const uint32_t id = P.vinc[p];
+      const uint32_t id = P.vinc[p] & P.id_mask;
       const unsigned long long k = P.wkey[id];
       if (k != 0 && crew_better(P.stream, r, k, id + P.id_base, bk, bid == kNoEdge ? kNoEdge : bid + P.id_base)) {
         bk = k;
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(kBlock) k_crew_argmax_mid(const CrewParams P, 
     unsigned long long bk = 0;
     uint32_t bid = kNoEdge;
     for (unsigned long long p = P.voff[v] + lane; p < P.voff[v + 1]; p += 32) {
-      const uint32_t id = P.vinc[p];
+      const uint32_t id = P.vinc[p] & P.id_mask;
       const unsigned long long k = P.wkey[id];
       if (k != 0) crew_combine(P, r, bk, bid, k, id);
     }
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kBlock) k_crew_argmax_hub(const CrewParams P, 
     unsigned long long bk = 0;
     uint32_t bid = kNoEdge;
     for (unsigned long long p = P.voff[v] + threadIdx.x; p < P.voff[v + 1]; p += kBlock) {
-      const uint32_t id = P.vinc[p];
+      const uint32_t id = P.vinc[p] & P.id_mask;
       const unsigned long long k = P.wkey[id];
       if (k != 0) crew_combine(P, r, bk, bid, k, id);
     }
@@ -279,7 +284,6 @@ void crew_release(Graph* g) {
   pool_free(c->ww8);
   pool_free(c->vlen);
   pool_free(c->alive);
-  pool_free(c->votes);
   pool_free(c->vnew);
   pool_free(c->gflag);
   pool_free(c->gclass);
@@ -293,6 +297,8 @@ void crew_release(Graph* g) {
   pool_free(c->task_len);
   pool_free(c->part_key);
   pool_free(c->part_id);
+  pool_free(c->lkey);
+  pool_free(c->mnow);
   delete c;
   g->crew = nullptr;
 }
@@ -351,6 +357,7 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
   P.stream.width = st->noise_high - st->noise_low;
   P.voff = reinterpret_cast<const unsigned long long*>(g->voff);
   P.vinc = g->vinc;
+  P.id_mask = g->vinc_flagged ? 0x7fffffffu : 0xffffffffu;
   P.wkey = c->wkey;
   P.estat = c->estat;
   P.top = c->top;
@@ -409,12 +416,34 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
 }
 
 #include "hlm_crew2.inc"
+#include "hlm_shard.inc"
 
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out, int report_variant) {
   const char* env = std::getenv("HLM_B200_CREW_SOFT");
-  // 16-bit vote lanes: an edge with more pins than that takes the soft-deletion form
-  if ((env && env[0] == '1') || g->max_edge_size > 65535u) return match_crew_soft(g, st, cfg, out, report_variant);
+  // the work-optimal form needs the first-pin flag of the incidence entries (bit 31: < 2^31 edges)
+  if ((env && env[0] == '1') || g->m >= 0x7fffffffu) return match_crew_soft(g, st, cfg, out, report_variant);
   return match_crew_compacting(g, st, cfg, out, report_variant);
 }
 
 }  // namespace hlmb
+
+using namespace hlmb;
+
+extern "C" {
+
+int hlm_b200_match_sharded(hlm_b200_graph* const* shards, int num_shards, hlm_b200_comm* comm,
+                           const hlm_b200_stream* stream, const hlm_b200_config* cfg, hlm_b200_result* results,
+                           hlm_b200_shard_report* report) {
+  return match_sharded(reinterpret_cast<Graph* const*>(shards), num_shards, reinterpret_cast<Comm*>(comm), stream, cfg,
+                       results, report);
+}
+
+void hlm_b200_shard_report_free(hlm_b200_shard_report* report) {
+  if (!report) return;
+  std::free(report->collective_bytes_per_round);
+  std::free(report->live_vertices_per_round);
+  report->collective_bytes_per_round = nullptr;
+  report->live_vertices_per_round = nullptr;
+}
+
+}  // extern "C"

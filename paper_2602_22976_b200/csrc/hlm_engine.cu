@@ -235,11 +235,9 @@ void Workspace::drop_graphs() {
   }
 }
 
-static void mg_release(Graph* g);
 
 Graph::~Graph() {
   cudaSetDevice(device);
-  mg_release(this);
   ws.release();
   crew_release(this);
   dev_free(pins);
@@ -438,6 +436,7 @@ struct PhaseTrace {
 struct UploadPlan {
   bool reorder = true;      // sort the resident edges by first pin (pays off after ~30 matchings)
   bool host_assist = true;  // use the host cores as described above
+  uint32_t id_base = 0;     // the rows are the edges [id_base, id_base + m) of a larger instance (a shard)
 };
 
 struct HostScan {
@@ -492,6 +491,7 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   };
   g->n = h->num_vertices;
   g->m = h->num_edges;
+  g->id_base = plan.id_base;
   const uint32_t m = g->m;
   g->kappa = m ? h->edge_offsets[m] : 0;
   if (m && h->edge_offsets[0] != 0) {
@@ -1383,6 +1383,14 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   return HLM_B200_OK;
 }
 
+// what HLM_B200_VARIANT_AUTO runs a resident instance on (and whether the loader sorts its edges by
+// first pin, which only the CRCW sweeps gain from)
+bool crcw_is_faster(const Graph* g) {
+  const uint64_t vtop_bytes = static_cast<uint64_t>(g->n) * 4, l2 = static_cast<uint64_t>(g->l2_bytes);
+  return g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
+         (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4);
+}
+
 int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
   std::memset(out, 0, sizeof(*out));
   if (!g || !st || !cfg) {
@@ -1416,9 +1424,7 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
       // once n * 4 B outgrows L2 (configs 3, 4, the config-5 shard shape).  HLM_B200_AUTO=crcw|crew.
       // Measured (device ms, crcw / crew): RMAT graphs 2^26 edges 2.3 / 4.6, 2^28 edges 6.2 / 15.1;
       // 4-uniform n = 1 M 0.45 / 0.49, n = 24 M 15.4 / 10.2, n = 32 M 15.1 / 8.8.
-      const uint64_t vtop_bytes = static_cast<uint64_t>(g->n) * 4, l2 = static_cast<uint64_t>(g->l2_bytes);
-      bool crcw = g->one_shot || g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
-                  (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4);
+      bool crcw = g->one_shot || crcw_is_faster(g);
       if (const char* env = std::getenv("HLM_B200_AUTO")) {
         if (std::strcmp(env, "crew") == 0) crcw = false;
         if (std::strcmp(env, "crcw") == 0) crcw = true;
@@ -1446,7 +1452,101 @@ int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, h
   return rc;
 }
 
-#include "hlm_multi.inc"
+
+// hlm_b200_match_host with cfg->num_gpus = k > 1: the edge rows are cut into k blocks, block i is
+// loaded as a shard on device (device + i) mod (visible devices), the shards are matched as one
+// instance (hlm_shard.inc) and the slices are concatenated -- ascending, because the blocks are.
+static int match_host_sharded(const hlm_b200_csr_view* h, const hlm_b200_stream* st, const hlm_b200_config* cfg,
+                              int device, hlm_b200_result* out) {
+  if (!h || (h->num_edges && (!h->edge_offsets || !h->base_weights))) {
+    set_error("null hypergraph arrays");
+    return HLM_B200_ERR_INPUT;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    set_error("no CUDA device");
+    return HLM_B200_ERR_CUDA;
+  }
+  const uint32_t m = h->num_edges;
+  const uint32_t k = std::max<uint32_t>(1, std::min<uint32_t>(cfg->num_gpus, std::max<uint32_t>(m, 1u)));
+  const uint32_t per = (m + k - 1) / k;
+  std::vector<Graph*> shards;
+  std::vector<hlm_b200_result> parts;
+  auto cleanup = [&]() {
+    for (Graph* g : shards) delete g;
+    for (auto& r : parts) hlm_b200_result_free(&r);
+  };
+  uint64_t h2d = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    const uint32_t b = std::min<uint64_t>(m, static_cast<uint64_t>(i) * per), cnt = std::min(m, b + per) - b;
+    if (cnt == 0 && m != 0) continue;
+    std::vector<uint64_t> off(static_cast<size_t>(cnt) + 1);
+    const uint64_t o0 = m ? h->edge_offsets[b] : 0;
+    for (uint32_t e = 0; e <= cnt && m; ++e) off[e] = h->edge_offsets[b + e] - o0;
+    hlm_b200_csr_view v = *h;
+    v.vertex_offsets = nullptr;
+    v.vertex_incidence = nullptr;
+    v.num_edges = cnt;
+    v.edge_offsets = off.data();
+    v.edge_members = h->edge_members ? h->edge_members + o0 : nullptr;
+    v.base_weights = h->base_weights ? h->base_weights + b : nullptr;
+    UploadPlan plan;
+    plan.reorder = false;
+    plan.id_base = b;
+    Graph* g = nullptr;
+    const int rc = upload(&v, (device + static_cast<int>(i)) % ndev, &g, plan);
+    if (rc != HLM_B200_OK) {
+      cleanup();
+      return rc;
+    }
+    g->one_shot = true;
+    h2d += g->h2d_bytes;
+    shards.push_back(g);
+  }
+  parts.resize(shards.size());
+  for (auto& r : parts) std::memset(&r, 0, sizeof(r));
+  hlm_b200_shard_report rep;
+  int rc = match_sharded(shards.data(), static_cast<int>(shards.size()), nullptr, st, cfg, parts.data(), &rep);
+  if (rc == HLM_B200_OK || rc == HLM_B200_ERR_ROUND_LIMIT) {
+    uint64_t total = 0;
+    for (auto& r : parts) total += r.num_matched;
+    const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
+    const uint32_t rounds = parts[0].rounds;
+    out->matched_edges = static_cast<uint32_t*>(host_result_alloc(sizeof(uint32_t) * (total + 1)));
+    out->matched_round = want_round ? static_cast<uint16_t*>(host_result_alloc(sizeof(uint16_t) * (total + 1))) : nullptr;
+    out->per_round_matched = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
+    out->per_round_deactivated = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
+    if (!out->matched_edges || (want_round && !out->matched_round) || !out->per_round_matched || !out->per_round_deactivated) {
+      set_error("host allocation of the result failed");
+      rc = HLM_B200_ERR_NOMEM;
+    } else {
+      uint64_t at = 0;
+      for (auto& r : parts) {
+        if (r.num_matched) std::memcpy(out->matched_edges + at, r.matched_edges, r.num_matched * 4);
+        if (want_round && r.num_matched && r.matched_round) std::memcpy(out->matched_round + at, r.matched_round, r.num_matched * 2);
+        at += r.num_matched;
+        out->total_edge_visits += r.total_edge_visits;
+        out->total_pin_visits += r.total_pin_visits;
+        out->device_edge_visits += r.device_edge_visits;
+        out->kernel_launches += r.kernel_launches;
+        out->device_ms = std::max(out->device_ms, r.device_ms);
+      }
+      out->num_matched = total;
+      out->rounds = rounds;
+      for (uint32_t q = 0; q < rounds; ++q) {
+        out->per_round_matched[q] = parts[0].per_round_matched[q];
+        out->per_round_deactivated[q] = parts[0].per_round_deactivated[q];
+      }
+      out->total_weight = parts[0].total_weight;
+      out->wall_time_ms = parts[0].wall_time_ms;
+      out->tie_redo_rounds = rep.tie_redo_rounds;
+      out->h2d_bytes = h2d;
+    }
+    hlm_b200_shard_report_free(&rep);
+  }
+  cleanup();
+  return rc;
+}
 
 // ---------------------------------------------------------------------------------------------
 // verify_matching (exact.hpp:115-140)
@@ -1544,6 +1644,21 @@ int hlm_b200_graph_upload(const hlm_b200_csr_view* host, int device, hlm_b200_gr
   return rc;
 }
 
+int hlm_b200_graph_upload_shard(const hlm_b200_csr_view* rows, uint32_t edge_begin, int device, hlm_b200_graph** out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  if (rows && static_cast<uint64_t>(edge_begin) + rows->num_edges > 0xffffffffull) {
+    set_error("edge ids are 32-bit: shard [%u, %u + %u)", edge_begin, edge_begin, rows->num_edges);
+    return HLM_B200_ERR_INPUT;
+  }
+  UploadPlan plan;
+  plan.reorder = false;  // vertex ids must mean the same on every shard
+  plan.id_base = edge_begin;
+  Graph* g = nullptr;
+  const int rc = upload(rows, device, &g, plan);
+  *out = reinterpret_cast<hlm_b200_graph*>(g);
+  return rc;
+}
+
 int hlm_b200_graph_generate(const hlm_b200_syn_spec* spec, int device, hlm_b200_graph** out) {
   if (!out || !spec) return HLM_B200_ERR_INPUT;
   Graph* g = nullptr;
@@ -1599,6 +1714,7 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
     set_error("null argument");
     return HLM_B200_ERR_INPUT;
   }
+  if (cfg->num_gpus > 1) return match_host_sharded(host, stream, cfg, device, out);
   Graph* g = nullptr;
   UploadPlan plan;
   plan.reorder = false;  // a single matching does not repay the 40 ms first-pin sort (9.2 vs 7.9 ms)
@@ -1618,50 +1734,6 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   delete g;
   tr.mark("match_host: release");
   return rc;
-}
-
-uint64_t hlm_b200_mg_exch_words(uint32_t num_vertices) { return mg_exch_words(num_vertices); }
-
-int hlm_b200_graph_weight_info(hlm_b200_graph* gh, double noise_low, hlm_b200_weight_info* info) {
-  if (!gh || !info) return HLM_B200_ERR_INPUT;
-  Graph* g = reinterpret_cast<Graph*>(gh);
-  CU_CHECK(cudaSetDevice(g->device));
-  info->base_min = g->base_min;
-  info->base_max = g->base_max;
-  if (g->base && g->m) {
-    WeightStats ws;
-    ST_CHECK(weight_stats(g, noise_low, &ws));
-    info->non_integer = ws.non_integer ? 1 : 0;
-  } else {
-    const double w = g->base_const + noise_low;
-    info->non_integer = (w == std::floor(w) && w < 4294967296.0) ? 0 : 1;
-  }
-  info->num_edges = g->m;
-  return HLM_B200_OK;
-}
-
-int hlm_b200_mg_begin(hlm_b200_graph* g, const hlm_b200_stream* stream, const hlm_b200_config* cfg,
-                      const hlm_b200_mg_setup* setup) {
-  if (!g || !stream || !cfg) return HLM_B200_ERR_INPUT;
-  return mg_begin(reinterpret_cast<Graph*>(g), stream, cfg, setup);
-}
-int hlm_b200_mg_vertex_max(hlm_b200_graph* g) { return mg_vertex_max(reinterpret_cast<Graph*>(g)); }
-int hlm_b200_mg_claims(hlm_b200_graph* g) { return mg_claims(reinterpret_cast<Graph*>(g)); }
-int hlm_b200_mg_decide(hlm_b200_graph* g, uint32_t* global_active, int* tie) {
-  if (!global_active || !tie) return HLM_B200_ERR_INPUT;
-  return mg_decide(reinterpret_cast<Graph*>(g), global_active, tie);
-}
-int hlm_b200_mg_check_commit(hlm_b200_graph* g) { return mg_check_commit(reinterpret_cast<Graph*>(g)); }
-int hlm_b200_mg_exact_level(hlm_b200_graph* g, int level, void* va, void* vb, void* vc) {
-  return mg_exact_level(reinterpret_cast<Graph*>(g), level, va, vb, vc);
-}
-int hlm_b200_mg_end_round(hlm_b200_graph* g, uint32_t global_active, int* status) {
-  if (!status) return HLM_B200_ERR_INPUT;
-  return mg_end_round(reinterpret_cast<Graph*>(g), global_active, status);
-}
-int hlm_b200_mg_finish(hlm_b200_graph* g, double weight_before, hlm_b200_result* out) {
-  if (!out) return HLM_B200_ERR_INPUT;
-  return mg_finish(reinterpret_cast<Graph*>(g), weight_before, out);
 }
 
 void hlm_b200_result_free(hlm_b200_result* r) {

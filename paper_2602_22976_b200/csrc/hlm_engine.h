@@ -91,12 +91,12 @@ struct Graph {
   // vertex -> incident edges, built on the device when a variant (crew) or a download needs it
   uint64_t* voff = nullptr;  // n+1
   uint32_t* vinc = nullptr;  // kappa
+  bool vinc_flagged = false;  // bit 31 of an entry: the list's vertex is the first pin of that edge (m < 2^31)
   uint64_t device_bytes = 0;
   uint64_t h2d_bytes = 0;
   int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0;
   Workspace ws;
   CrewState* crew = nullptr;
-  void* mg = nullptr;  // MgState of an edge-partitioned run in progress (hlm_multi.inc)
   EdgeCsr csr() const;
   ~Graph();
 };
@@ -122,6 +122,7 @@ int ensure_workspace(Graph* g, uint32_t max_rounds);
 bool reorder_enabled();
 bool renumber_enabled();
 int reorder_by_first_pin(Graph* g);
+bool crcw_is_faster(const Graph* g);
 int renumber_by_degree(Graph* g);
 int build_base_codes(Graph* g);
 int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins);
@@ -131,6 +132,9 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out,
                int report_variant = HLM_B200_VARIANT_CREW);
 void crew_release(Graph* g);
+struct Comm;  // hlm_comm.h
+int match_sharded(Graph* const* graphs, int num_shards, Comm* comm, const hlm_b200_stream* st, const hlm_b200_config* cfg,
+                  hlm_b200_result* results, hlm_b200_shard_report* report);
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
                     hlm_b200_result* out, double weight_before = 0.0);
 int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out, uint64_t count,

@@ -1393,75 +1393,3 @@ __global__ void k_gather_weights(const double* base, const uint32_t* ids, uint32
 }
 
 }  // namespace hlmb
-
-// ---------------------------------------------------------------------------------------------
-// Multi-GPU (edge-partitioned) helpers.  Each rank runs the same round kernels on its shard; the
-// per-vertex maxima are combined with an all-reduce(max) over vkey between the vertex-max pass
-// and the check, newly dead vertices with an all-reduce(sum) over a bitmap (matched edges are
-// vertex-disjoint across the whole instance, so every bit is set by exactly one rank and the sum
-// is a bitwise OR).  A vertex whose maximum key is held by edges of two different ranks cannot
-// be seen by the local returning atomicMax; the claimant count (4 bits per vertex, summed over
-// ranks) detects it and sends the round to the exact three-level path.
-// ---------------------------------------------------------------------------------------------
-namespace hlmb {
-
-__global__ void k_mg_refresh_top(const unsigned long long* vkey, uint32_t* vtop, uint32_t n) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    if (vtop[v] != kTopDead) vtop[v] = static_cast<uint32_t>(vkey[v] >> 32);
-}
-
-__device__ __forceinline__ void mg_claim_edge(const RoundParams& P, uint32_t e, uint32_t r, uint32_t tag,
-                                              uint32_t* claims, uint32_t first_lane, uint32_t stride) {
-  uint64_t b;
-  uint32_t s;
-  P.csr.range(e, b, s);
-  const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, e), r, base_of(P, e), tag);
-  for (uint32_t i = first_lane; i < s; i += stride) {
-    const uint32_t v = __ldg(P.csr.pins + b + i);
-    if (__ldcg(P.vkey + v) == key) atomicAdd(claims + (v >> 3), 1u << ((v & 7u) * 4u));
-  }
-}
-
-// every local edge that holds the (global) maximum at one of its pins claims that vertex
-__global__ void __launch_bounds__(kBlock) k_mg_claims(const RoundParams P, uint32_t* claims) {
-  const Ctrl* c = P.ctrl;
-  const uint32_t r = c->round;
-  const uint32_t tag = round_tag(P.ks, r);
-  const uint64_t slots = static_cast<uint64_t>(P.nseg) * P.seg_cap;
-  for (uint64_t pos = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; pos < slots;
-       pos += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t seg = static_cast<uint32_t>(pos / P.seg_cap);
-    if (static_cast<uint32_t>(pos % P.seg_cap) >= P.cand_cnt[seg]) continue;
-    mg_claim_edge(P, P.cand_ids[pos], r, tag, claims, 0, 1);
-  }
-  // large edges: one warp per edge of the current list
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
-  for (uint32_t pos = warp; pos < P.num_large; pos += nwarps)
-    if (P.large_state[pos] != LARGE_DROPPED) mg_claim_edge(P, P.large_ids[pos], r, tag, claims, lane, 32);
-}
-
-// any vertex claimed twice?  (a nibble >= 2 has one of its three upper bits set)
-__global__ void k_mg_tie_scan(const uint32_t* claims, uint64_t words, uint32_t* flag) {
-  bool any = false;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < words;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    any |= (claims[i] & 0xEEEEEEEEu) != 0u;
-  if (any) *flag = 1u;
-}
-
-__global__ void k_mg_apply_dead(const uint32_t* dead_new, uint32_t words, uint32_t* vtop, uint32_t n,
-                                uint32_t* dead_all) {
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
-    uint32_t bits = dead_new[w];
-    if (bits) dead_all[w] |= bits;
-    while (bits) {
-      const uint32_t v = w * 32u + (__ffs(bits) - 1u);
-      bits &= bits - 1u;
-      if (v < n) vtop[v] = kTopDead;
-    }
-  }
-}
-
-}  // namespace hlmb

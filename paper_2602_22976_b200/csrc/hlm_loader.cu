@@ -4,6 +4,7 @@
 //   * the vertex-incidence CSR builder (counting sort of pins by vertex; the device analogue of
 //     hypergraph.hpp:144-151),
 //   * exclusive scan, download.
+#include <cub/device/device_segmented_sort.cuh>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -176,8 +177,10 @@ __global__ void k_copy_u64(const unsigned long long* in, uint64_t count, unsigne
 }
 
 // pos[v] starts as voff[v]; the returning 64-bit add hands out the slots of v's list
+// flag_first: bit 31 of the entry written for an edge's FIRST pin is set (the vertex-owned matching
+// kernels use it to decide for free whether a vertex is the first pin of its argmax)
 __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, uint32_t vhi, unsigned long long* pos,
-                                 const uint32_t* orig, uint32_t* vinc) {
+                                 const uint32_t* orig, uint32_t* vinc, bool flag_first) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     uint64_t b;
     uint32_t s;
@@ -187,13 +190,13 @@ __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, ui
       const uint32_t v = __ldcs(csr.pins + b + i);
       if (v < vlo || v >= vhi) continue;
       if (id == 0xffffffffu) id = orig ? orig[e] : e;
-      vinc[atomicAdd(pos + v, 1ull)] = id;
+      vinc[atomicAdd(pos + v, 1ull)] = (flag_first && i == 0) ? (id | 0x80000000u) : id;
     }
   }
 }
 
 // voff (n+1) / vinc (kappa) of the CSR `csr` over n vertices; edges are named by orig[] when given
-static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc) {
+static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc, bool flag_first = false) {
   cudaStream_t s = g->stream;
   const bool trace = std::getenv("HLM_B200_TRACE") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
@@ -230,7 +233,7 @@ static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, ui
     for (uint64_t lo = 0; lo < g->n; lo += win8)
       k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(csr, g->m, static_cast<uint32_t>(lo),
                                                            static_cast<uint32_t>(std::min<uint64_t>(g->n, lo + win8)), pos,
-                                                           g->orig, vinc);
+                                                           g->orig, vinc, flag_first);
     CU_CHECK(cudaStreamSynchronize(s));
     mark("fill");
     pool_free(pos);
@@ -247,7 +250,8 @@ int build_incidence(Graph* g) {
   ST_CHECK(dalloc(&g->vinc, g->kappa + 4));  // one quad of padding: the CREW sweep loads 16 bytes at a time
   g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
   CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 16, g->stream));
-  return build_incidence_into(g, g->csr(), g->voff, g->vinc);
+  g->vinc_flagged = g->m < 0x7fffffffu;
+  return build_incidence_into(g, g->csr(), g->voff, g->vinc, g->vinc_flagged);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -488,6 +492,32 @@ __global__ void k_fill_const(double* out, uint32_t m, double v) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) out[e] = v;
 }
 
+// ascending edge ids inside every vertex's list (cub segmented sort; not on the matching path)
+static int sort_incidence_lists(Graph* g, const uint64_t* voff, uint32_t** vinc) {
+  cudaStream_t s = g->stream;
+  uint32_t* sorted = nullptr;
+  ST_CHECK(dalloc(&sorted, g->kappa + 1));
+  const unsigned long long* off = reinterpret_cast<const unsigned long long*>(voff);
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, *vinc, sorted, static_cast<int64_t>(g->kappa),
+                                                     static_cast<int64_t>(g->n), off, off + 1, s);
+  void* tmp = nullptr;
+  if (e == cudaSuccess) e = pool_malloc(&tmp, std::max<size_t>(tmp_bytes, 16));
+  if (e == cudaSuccess)
+    e = cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, *vinc, sorted, static_cast<int64_t>(g->kappa),
+                                           static_cast<int64_t>(g->n), off, off + 1, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  pool_free(tmp);
+  if (e != cudaSuccess) {
+    pool_free(sorted);
+    set_error("sorting the incidence lists failed: %s", cudaGetErrorString(e));
+    return HLM_B200_ERR_CUDA;
+  }
+  pool_free(*vinc);
+  *vinc = sorted;
+  return HLM_B200_OK;
+}
+
 int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t* pins, double* base) {
   CU_CHECK(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
@@ -526,21 +556,21 @@ int download(Graph* g, uint64_t* voff, uint32_t* vinc, uint64_t* eoff, uint32_t*
     const uint32_t* d_vinc = nullptr;
     uint64_t* t_voff = nullptr;
     uint32_t* t_vinc = nullptr;
-    if (old_pins) {  // renumbered instance: the incidence side in the caller's numbering is built on the fly
+    // Built on the fly in the caller's numbering and without the first-pin flags of the resident copy;
+    // every list is then sorted ascending, which is what build_hypergraph (hypergraph.hpp:128-133)
+    // produces (the slot fill by atomics leaves the order inside a list to chance).
+    {
       int rc = dalloc(&t_voff, static_cast<size_t>(g->n) + 1);
-      if (rc == HLM_B200_OK) rc = dalloc(&t_vinc, g->kappa);
+      if (rc == HLM_B200_OK) rc = dalloc(&t_vinc, g->kappa + 1);
       if (rc == HLM_B200_OK) {
         EdgeCsr csr = g->csr();
-        csr.pins = old_pins;
+        if (old_pins) csr.pins = old_pins;
         rc = build_incidence_into(g, csr, t_voff, t_vinc);
       }
+      if (rc == HLM_B200_OK && vinc && g->kappa) rc = sort_incidence_lists(g, t_voff, &t_vinc);
       if (rc != HLM_B200_OK) return pool_free(old_pins), pool_free(t_voff), pool_free(t_vinc), rc;
       d_voff = t_voff;
       d_vinc = t_vinc;
-    } else {
-      ST_CHECK(build_incidence(g));
-      d_voff = g->voff;
-      d_vinc = g->vinc;
     }
     if (voff) CU_CHECK(cudaMemcpyAsync(voff, d_voff, (static_cast<size_t>(g->n) + 1) * 8, cudaMemcpyDeviceToHost, s));
     if (vinc && g->kappa) CU_CHECK(cudaMemcpyAsync(vinc, d_vinc, g->kappa * 4, cudaMemcpyDeviceToHost, s));
@@ -605,6 +635,10 @@ __global__ void k_unpermute_rows(const uint32_t* pins, const uint32_t* orig, uin
 
 int reorder_by_first_pin(Graph* g) {
   if (g->orig || !g->uniform_d || g->m < 2) return HLM_B200_OK;
+  // Only the CRCW sweeps gain from the order (coalesced first-pin filter words).  The vertex-owned
+  // kernels look an edge's row up by its caller id: on a sorted instance that is one more random
+  // read per candidate (id -> row), so instances they will run are left in the caller's order.
+  if (!crcw_is_faster(g) && !std::getenv("HLM_B200_FORCE_REORDER")) return HLM_B200_OK;
   cudaStream_t s = g->stream;
   const uint32_t m = g->m, d = g->uniform_d;
   uint32_t *cnt = nullptr, *new_pins = nullptr, *orig = nullptr;

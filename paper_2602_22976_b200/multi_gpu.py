@@ -1,24 +1,24 @@
 """Edge-partitioned matching across GPUs (BASELINE config 5).
 
-One process per GPU holds a contiguous block of edge rows (global edge ids) plus replicated
-per-vertex arrays.  Each round the ranks run the same sm_100a kernels on their shard through the
-step-level C-ABI (csrc/hlm_multi.inc) and combine three arrays with collectives:
+One process per GPU holds a contiguous block of edge rows (global edge ids) and the incidence lists of
+its own edges; per-vertex state is replicated.  The round loop, the collectives (NCCL, bound by the
+library at run time) and the tie handling all live inside libhlm_b200.so behind ONE call,
+hlm_b200_match_sharded (csrc/hlm_shard.inc has the protocol).  Per round the ranks combine
 
-    vkey[n]  int64   all-reduce(max)   the vertex maxima             (8 n bytes)
-    claims   int32   all-reduce(sum)   claimants per vertex, 4 bits  (n / 2 bytes) + 8 words of stats
-    dead_new int32   all-reduce(sum)   newly covered vertices        (n / 8 bytes; each bit is set
-                                       by exactly one rank because matched edges are disjoint, so
-                                       the sum is a bitwise OR -- NCCL has no OR)
+    lkey[L_r]  uint64  all-reduce(max)   local maxima of the L_r still-live vertices   (8 L_r bytes)
+    covered    uint32  all-reduce(sum)   newly covered vertices + 8 statistics words    (n / 8 bytes;
+                                         bits are disjoint over ranks, so the sum is an OR)
+    alive      uint32  all-reduce(sum)   4 words: alive edges (termination)
 
-The result is identical for every rank count (the reference's invariant "independent of workers",
-test_par.cpp:32-55): priorities use global edge ids, and a vertex whose maximum is claimed by two
-edges (on the same or on different ranks) sends that round to the exact three-level comparator,
-whose levels are all-reduced as well.
+and the host waits for the device once per round.  The result is identical for every rank count (the
+reference's invariant "independent of workers", test_par.cpp:32-55): priorities use global edge ids,
+and a vertex whose maximum weight sits on two ranks sends the round through the reference comparator
+level by level (tie hash, then id), each level all-reduced.
 
-`ShardedMatcher` drives a LIST of shards held by this process plus an optional torch.distributed
-group: a list of k shards with no group is k "virtual ranks" on one GPU (how the protocol is
-tested on a single B200); one shard per process with an NCCL group is the production layout.
-Python only orchestrates: every array operation is a CUDA kernel of the library or a collective.
+Python here is plumbing only: it makes the communicator (torch.distributed carries the 128-byte NCCL
+id to the other ranks) and marshals the call.  Several shards handed over by ONE process and sitting
+on one GPU are "virtual ranks": the same kernels and the same loop, which is how the path is tested
+on a single B200.
 """
 from __future__ import annotations
 
@@ -34,9 +34,6 @@ from . import _lib
 from .api import (DeviceHypergraph, MatchResult, Matching, ParallelConfig, RoundLimitError, RunReport,
                   WeightStream, WorkCounters, _raise, _take)
 
-MG_RUNNING, MG_DONE, MG_ROUND_LIMIT = 0, 1, 2
-
-
 def shard_bounds(num_edges: int, world: int, rank: int):
     """Block partition of the edge ids: rank r owns [begin, begin + count)."""
     per = (num_edges + world - 1) // world
@@ -44,344 +41,150 @@ def shard_bounds(num_edges: int, world: int, rank: int):
     return begin, min(num_edges, begin + per) - begin
 
 
-class Collectives:
-    """All-reduce over the shards of this process and, if given, a torch.distributed group."""
+class Communicator:
+    """One rank of the NCCL communicator the library's round driver uses (hlm_b200_comm).  The 128-byte
+    unique id is made by rank 0 and shipped to the others by whatever the caller has -- here a
+    torch.distributed broadcast; the data path itself never goes through torch."""
 
-    def __init__(self, dist=None, group=None):
-        self.dist = dist
-        self.group = group
-        self.bytes_moved = 0
+    def __init__(self, handle, rank: int, world: int):
+        self._h, self.rank, self.world = handle, rank, world
 
-    def _reduce(self, tensors, op_local, op_dist):
-        acc = tensors[0]
-        if len(tensors) > 1:
-            acc = tensors[0].clone()
-            for t in tensors[1:]:
-                op_local(acc, t)
-        if self.dist is not None:
-            self.dist.all_reduce(acc, op=op_dist, group=self.group)
-            self.bytes_moved += acc.numel() * acc.element_size()
-        if len(tensors) > 1 or self.dist is not None:
-            for t in tensors:
-                if t is not acc:
-                    t.copy_(acc)
-
-    def allreduce_max(self, tensors):
+    @staticmethod
+    def exchange_unique_id(dist, make_id, group=None) -> bytes:
+        """rank 0: make_id() -> 128 bytes; everyone: the same bytes (any backend)."""
         import torch
 
-        self._reduce(tensors, lambda a, b: torch.maximum(a, b, out=a),
-                     self.dist.ReduceOp.MAX if self.dist is not None else None)
+        rank = dist.get_rank(group)
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        buf = torch.zeros(_lib.UNIQUE_ID_BYTES, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            raw = make_id()
+            assert len(raw) == _lib.UNIQUE_ID_BYTES
+            buf.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+        dist.broadcast(buf, src=0, group=group)
+        return bytes(buf.cpu().numpy().tobytes())
 
-    def allreduce_sum(self, tensors):
-        self._reduce(tensors, lambda a, b: a.add_(b), self.dist.ReduceOp.SUM if self.dist is not None else None)
+    @classmethod
+    def from_torch(cls, dist, device: int, group=None) -> "Communicator":
+        lib = _lib.load_library()
 
-    def reduce_scalars(self, values: List[float], op: str) -> float:
-        """op in {'min', 'max', 'sum'} over the local values and the group."""
-        import torch
+        def make_id():
+            raw = (C.c_uint8 * _lib.UNIQUE_ID_BYTES)()
+            st = lib.hlm_b200_comm_unique_id(raw)
+            if st != _lib.OK:
+                _raise(st, "hlm_b200_comm_unique_id")
+            return bytes(raw)
 
-        local = {"min": min, "max": max, "sum": sum}[op](values)
-        if self.dist is None:
-            return local
-        t = torch.tensor([local], dtype=torch.float64, device="cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu")
-        self.dist.all_reduce(t, op={"min": self.dist.ReduceOp.MIN, "max": self.dist.ReduceOp.MAX,
-                                    "sum": self.dist.ReduceOp.SUM}[op], group=self.group)
-        return float(t.item())
+        uid = cls.exchange_unique_id(dist, make_id, group)
+        return cls.create(uid, dist.get_rank(group), dist.get_world_size(group), device)
 
-    def chain_weights(self, fold):
-        """Ordered fold across ranks: rank k starts from the total of ranks < k (the reference sums
-        base weights in ascending edge-id order).  `fold(acc_in) -> acc_out` is this process's part."""
-        if self.dist is None:
-            return fold(0.0)
-        import torch
-
-        rank, world = self.dist.get_rank(self.group), self.dist.get_world_size(self.group)
-        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
-        acc = torch.zeros(1, dtype=torch.float64, device=dev)
-        out = 0.0
-        for k in range(world):
-            if rank == k:
-                out = fold(float(acc.item()))
-                acc[0] = out
-            self.dist.broadcast(acc, src=k, group=self.group)
-        return float(acc.item())
-
-    def gather_arrays(self, arr: np.ndarray) -> Optional[np.ndarray]:
-        """Concatenation of `arr` over ranks in rank order (every rank gets it)."""
-        if self.dist is None:
-            return arr
-        import torch
-
-        world = self.dist.get_world_size(self.group)
-        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
-        n = torch.tensor([arr.size], dtype=torch.int64, device=dev)
-        sizes = [torch.zeros_like(n) for _ in range(world)]
-        self.dist.all_gather(sizes, n, group=self.group)
-        sizes = [int(x.item()) for x in sizes]
-        cap = max(sizes) if sizes else 0
-        buf = torch.zeros(max(cap, 1), dtype=torch.int64, device=dev)
-        buf[:arr.size] = torch.from_numpy(arr.astype(np.int64)).to(dev)
-        parts = [torch.zeros_like(buf) for _ in range(world)]
-        self.dist.all_gather(parts, buf, group=self.group)
-        return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)]).astype(arr.dtype)
-
-
-class LibEngine:
-    """The production step engine: one shard on one GPU, driven through the C-ABI."""
-
-    def __init__(self, shard: DeviceHypergraph, stream=None):
-        import torch
-
-        self.shard = shard
-        self.lib = _lib.load_library()
-        info = shard.info()
-        self.n = int(info.num_vertices)
-        self.m_local = int(info.num_edges)
-        self.device = torch.device("cuda", int(info.device))
-        self.torch = torch
-        self.nw = (self.n + 31) // 32
-        self.nc = (self.n + 7) // 8
-        words = int(self.lib.hlm_b200_mg_exch_words(self.n))
-        with torch.cuda.device(self.device):
-            self.vkey = torch.zeros(self.n, dtype=torch.int64, device=self.device)
-            self.exch = torch.zeros(words, dtype=torch.int32, device=self.device)
-            # all shards of one process share one stream: library kernels, torch element-wise ops
-            # and the NCCL collectives are then ordered without host synchronisation
-            self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
-        self.exact = None
-        shard.set_stream(self.stream.cuda_stream)
-
-    # views the collectives act on
-    def keys(self):
-        return self.vkey
-
-    def claims_and_stats(self):
-        return self.exch[self.nw:]
-
-    def dead_new(self):
-        return self.exch[:self.nw]
-
-    def _ck(self, st, what):
+    @classmethod
+    def create(cls, uid: Optional[bytes], rank: int, world: int, device: int) -> "Communicator":
+        lib = _lib.load_library()
+        out = C.c_void_p()
+        raw = (C.c_uint8 * _lib.UNIQUE_ID_BYTES).from_buffer_copy(uid) if uid is not None else None
+        st = lib.hlm_b200_comm_create(raw, rank, world, device, C.byref(out))
         if st != _lib.OK:
-            _raise(st, what)
+            _raise(st, "hlm_b200_comm_create")
+        return cls(out.value, rank, world)
 
-    def weight_info(self, noise_low: float):
-        wi = _lib.WeightInfo()
-        self._ck(self.lib.hlm_b200_graph_weight_info(self.shard._h, noise_low, C.byref(wi)), "weight_info")
-        return wi.base_min, wi.base_max, int(wi.non_integer), int(wi.num_edges)
+    def nccl_version(self) -> int:
+        v = C.c_int(0)
+        _lib.load_library().hlm_b200_comm_info(self._h, None, None, None, C.byref(v))
+        return int(v.value)
 
-    def begin(self, stream: WeightStream, cfg: ParallelConfig, base_min, base_max, non_integer, m_global):
-        cs, cc = stream._c(), cfg._c()
-        su = _lib.MgSetup(self.vkey.data_ptr(), self.exch.data_ptr(), base_min, base_max, non_integer, m_global)
-        self._ck(self.lib.hlm_b200_mg_begin(self.shard._h, C.byref(cs), C.byref(cc), C.byref(su)), "mg_begin")
+    def destroy(self):
+        if self._h:
+            _lib.load_library().hlm_b200_comm_destroy(self._h)
+            self._h = None
 
-    def vertex_max(self):
-        self._ck(self.lib.hlm_b200_mg_vertex_max(self.shard._h), "mg_vertex_max")
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
 
-    def claims(self):
-        self._ck(self.lib.hlm_b200_mg_claims(self.shard._h), "mg_claims")
 
-    def decide(self):
-        act, tie = C.c_uint32(0), C.c_int(0)
-        self._ck(self.lib.hlm_b200_mg_decide(self.shard._h, C.byref(act), C.byref(tie)), "mg_decide")
-        return int(act.value), bool(tie.value)
-
-    def check_commit(self):
-        self._ck(self.lib.hlm_b200_mg_check_commit(self.shard._h), "mg_check_commit")
-
-    def exact_arrays(self):
-        if self.exact is None:
-            t = self.torch
-            with t.cuda.device(self.device):
-                self.exact = (t.zeros(self.n, dtype=t.int64, device=self.device),
-                              t.zeros(self.n, dtype=t.int64, device=self.device),
-                              t.zeros(self.n, dtype=t.int32, device=self.device))
-        return self.exact
-
-    def exact_level(self, level: int):
-        va, vb, vc = self.exact_arrays()
-        self._ck(self.lib.hlm_b200_mg_exact_level(self.shard._h, level, va.data_ptr(), vb.data_ptr(), vc.data_ptr()),
-                 "mg_exact_level")
-
-    def end_round(self, global_active: int) -> int:
-        status = C.c_int(0)
-        self._ck(self.lib.hlm_b200_mg_end_round(self.shard._h, global_active, C.byref(status)), "mg_end_round")
-        return int(status.value)
-
-    def finish(self, weight_before: float):
-        res = _lib.Result()
-        st = self.lib.hlm_b200_mg_finish(self.shard._h, weight_before, C.byref(res))
+def match_sharded(shards: List[DeviceHypergraph], stream: WeightStream, cfg: Optional[ParallelConfig] = None,
+                  comm: Optional[Communicator] = None):
+    """hlm_b200_match_sharded: the round loop, the collectives and the tie handling run inside the library.
+    Returns (MatchResult over the LOCAL slices concatenated -- global ids, global rounds / per-round
+    counts / total_weight --, shard report as a dict)."""
+    cfg = cfg or ParallelConfig()
+    lib = _lib.load_library()
+    k = len(shards)
+    handles = (C.c_void_p * k)(*[s._h for s in shards])
+    results = (_lib.Result * k)()
+    rep = _lib.ShardReport()
+    cs, cc = stream._c(), cfg._c()
+    st = lib.hlm_b200_match_sharded(handles, k, comm._h if comm else None, C.byref(cs), C.byref(cc), results,
+                                    C.byref(rep))
+    try:
         if st not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
-            _raise(st, "mg_finish")
-        out = dict(matched=_take(res.matched_edges, res.num_matched, np.uint32),
-                   round_of=_take(res.matched_round, res.num_matched, np.uint16),
-                   per_round_matched=_take(res.per_round_matched, res.rounds, np.uint32).astype(np.int64),
-                   per_round_deactivated=_take(res.per_round_deactivated, res.rounds, np.uint32).astype(np.int64),
-                   rounds=int(res.rounds), total_weight=float(res.total_weight), launches=int(res.kernel_launches),
-                   tie_redos=int(res.tie_redo_rounds), limit=st == _lib.ERR_ROUND_LIMIT)
-        self.lib.hlm_b200_result_free(C.byref(res))
-        return out
-
-    def sync(self):
-        self.stream.synchronize()
-
-
-class ShardedMatcher:
-    """run_variant over an edge-partitioned instance.  `engines`: the shards of this process in
-    ascending edge-id order; `coll`: how arrays cross shards / ranks."""
-
-    def __init__(self, engines: list, num_edges_global: int, kappa_global: int, coll: Optional[Collectives] = None):
-        self.engines = engines
-        self.m = int(num_edges_global)
-        self.kappa = int(kappa_global)
-        self.coll = coll or Collectives()
-        self.timings = {}
-
-    def _all(self, name, *args):
-        return [getattr(e, name)(*args) for e in self.engines]
-
-    def _sync(self):
-        pass  # one stream per process orders everything (see LibEngine.__init__)
-
-    def match(self, stream: WeightStream, cfg: Optional[ParallelConfig] = None, gather: bool = True) -> MatchResult:
-        cuda_stream = getattr(self.engines[0], "stream", None)
-        if cuda_stream is None:
-            return self._match(stream, cfg, gather)
-        import torch
-
-        with torch.cuda.stream(cuda_stream):
-            return self._match(stream, cfg, gather)
-
-    def _match(self, stream: WeightStream, cfg: Optional[ParallelConfig] = None, gather: bool = True) -> MatchResult:
-        cfg = cfg or ParallelConfig()
-        t0 = time.perf_counter()
-        E, coll = self.engines, self.coll
-        # 1. agree on the weight facts that fix the 64-bit key layout
-        infos = self._all("weight_info", stream.noise_low)
-        live = [i for i in infos if i[3] > 0] or infos
-        bmin = coll.reduce_scalars([i[0] for i in live], "min")
-        bmax = coll.reduce_scalars([i[1] for i in live], "max")
-        nonint = int(coll.reduce_scalars([float(i[2]) for i in infos], "max"))
-        self._all("begin", stream, cfg, bmin, bmax, nonint, self.m)
-        status, rounds_guard = MG_RUNNING, 0
-        t_coll = 0.0
-        while status == MG_RUNNING:
-            self._all("vertex_max")
-            self._sync()
-            tc = time.perf_counter()
-            coll.allreduce_max([e.keys() for e in E])
-            t_coll += time.perf_counter() - tc
-            self._all("claims")
-            self._sync()
-            tc = time.perf_counter()
-            coll.allreduce_sum([e.claims_and_stats() for e in E])
-            t_coll += time.perf_counter() - tc
-            decisions = self._all("decide")
-            active, tie = decisions[0]
-            assert all(d == decisions[0] for d in decisions), "ranks disagree after the all-reduce"
-            if active > 0:
-                if tie:
-                    self._exact_round()
-                else:
-                    self._all("check_commit")
-                    self._sync()
-            tc = time.perf_counter()
-            coll.allreduce_sum([e.dead_new() for e in E])
-            t_coll += time.perf_counter() - tc
-            statuses = self._all("end_round", active)
-            status = statuses[0]
-            assert all(s == status for s in statuses)
-            rounds_guard += 1
-            if rounds_guard > 70000:
-                raise RuntimeError("round loop did not terminate")
-        # 2. assemble: shards are in ascending id order, so concatenation is the sorted result
-        parts = []
-
-        def fold(acc):
-            for e in E:
-                p = e.finish(acc)
-                parts.append(p)
-                acc = p["total_weight"]
-            return acc
-
-        total_weight = coll.chain_weights(fold)
-        rounds = parts[0]["rounds"]
-        prm = np.sum([p["per_round_matched"] for p in parts], axis=0) if rounds else np.zeros(0, dtype=np.int64)
-        prd = np.sum([p["per_round_deactivated"] for p in parts], axis=0) if rounds else np.zeros(0, dtype=np.int64)
-        if coll.dist is not None and rounds:
-            import torch
-
-            dev = E[0].device if hasattr(E[0], "device") else "cpu"
-            t = torch.from_numpy(np.concatenate([prm, prd])).to(dev)
-            coll.dist.all_reduce(t, group=coll.group)
-            both = t.cpu().numpy()
-            prm, prd = both[:rounds], both[rounds:]
-        matched = np.concatenate([p["matched"] for p in parts]) if parts else np.zeros(0, dtype=np.uint32)
-        round_of = np.concatenate([p["round_of"] for p in parts]) if parts else np.zeros(0, dtype=np.uint16)
-        if gather:
-            matched = coll.gather_arrays(matched)
-            round_of = coll.gather_arrays(round_of)
-        wall = (time.perf_counter() - t0) * 1e3
-        self.timings = {"wall_ms": wall, "collective_ms": t_coll * 1e3, "collective_bytes": coll.bytes_moved}
-        matching = Matching(matched, total_weight, rounds, [int(x) for x in prm])
-        report = RunReport(rounds, [int(x) for x in prm], [int(x) for x in prd], round_of,
-                           WorkCounters(rounds, 3 * self.m * rounds, 3 * self.kappa * rounds), wall, 0, 0.0, 0,
-                           max(p["tie_redos"] for p in parts), sum(p["launches"] for p in parts), 0, matched)
-        if any(p["limit"] for p in parts):
-            raise RoundLimitError(matching, report)
-        return MatchResult(matching, report)
-
-    def _exact_round(self):
-        """Three max levels of the reference comparator, each all-reduced (weight_stream.hpp:105-113)."""
-        E, coll = self.engines, self.coll
-        arrays = [e.exact_arrays() for e in E]
-        for va, vb, vc in arrays:
-            va.zero_()
-            vb.zero_()
-            vc.zero_()
-        self._all("exact_level", 1)
-        self._sync()
-        coll.allreduce_max([a[0] for a in arrays])  # weight bits: positive doubles, < 2^63
-        self._all("exact_level", 2)
-        self._sync()
-        sign64 = -(1 << 63)
-        for _, vb, _ in arrays:  # unsigned order of the hash == signed order with the top bit flipped
-            vb.bitwise_xor_(sign64)
-        coll.allreduce_max([a[1] for a in arrays])
-        for _, vb, _ in arrays:
-            vb.bitwise_xor_(sign64)
-        self._all("exact_level", 3)
-        self._sync()
-        sign32 = -(1 << 31)
-        for _, _, vc in arrays:
-            vc.bitwise_xor_(sign32)
-        coll.allreduce_max([a[2] for a in arrays])
-        for _, _, vc in arrays:
-            vc.bitwise_xor_(sign32)
-        self._all("exact_level", 4)
-        self._sync()
+            _raise(st, "hlm_b200_match_sharded")
+        rounds = int(rep.rounds)
+        matched = np.concatenate([_take(r.matched_edges, r.num_matched, np.uint32) for r in results])
+        round_of = np.concatenate([_take(r.matched_round, r.num_matched, np.uint16) for r in results])
+        prm = _take(results[0].per_round_matched, rounds, np.uint32).tolist()
+        prd = _take(results[0].per_round_deactivated, rounds, np.uint32).tolist()
+        report = dict(rounds=rounds, num_local_shards=int(rep.num_local_shards), num_processes=int(rep.num_processes),
+                      tie_redo_rounds=int(rep.tie_redo_rounds), host_syncs=int(rep.host_syncs),
+                      kernel_launches=int(rep.kernel_launches), nccl_calls=int(rep.nccl_calls),
+                      num_edges_global=int(rep.num_edges_global), collective_bytes=int(rep.collective_bytes),
+                      collective_bytes_per_round=_take(rep.collective_bytes_per_round, rounds, np.uint64).tolist(),
+                      live_vertices_per_round=_take(rep.live_vertices_per_round, rounds, np.uint32).tolist())
+        matching = Matching(matched, float(results[0].total_weight), rounds, prm)
+        rr = RunReport(rounds, prm, prd, round_of,
+                       WorkCounters(rounds, sum(int(r.total_edge_visits) for r in results),
+                                    sum(int(r.total_pin_visits) for r in results)),
+                       float(results[0].wall_time_ms), 0, max(float(r.device_ms) for r in results), 0,
+                       int(rep.tie_redo_rounds), int(rep.kernel_launches), 0, matched)
+    finally:
+        for r in results:
+            lib.hlm_b200_result_free(C.byref(r))
+        lib.hlm_b200_shard_report_free(C.byref(rep))
+    if st == _lib.ERR_ROUND_LIMIT:
+        raise RoundLimitError(matching, rr)
+    return MatchResult(matching, rr), report
 
 
-def virtual_cluster(family: str, world: int, device: int = 0, **spec) -> ShardedMatcher:
-    """k edge shards of one synthetic instance on ONE GPU (no process group): the multi-GPU
-    protocol with the collectives replaced by element-wise ops between the shards' buffers."""
-    m = spec["m"]
-    import torch
-
-    engines, kappa = [], 0
-    shared = torch.cuda.Stream(device=torch.device("cuda", device))
+def generate_shards(family: str, world: int, device: int = 0, **spec) -> List[DeviceHypergraph]:
+    """k edge shards of one synthetic instance on ONE GPU ("virtual ranks")."""
+    out = []
     for r in range(world):
-        b, k = shard_bounds(m, world, r)
-        if k == 0:
+        b, k = shard_bounds(spec["m"], world, r)
+        if k:
+            out.append(DeviceHypergraph.generate(family, edge_begin=b, m_local=k, device=device, **spec))
+    return out
+
+
+def upload_shards(h, world: int, device: int = 0) -> List[DeviceHypergraph]:
+    """The edge rows of a host Hypergraph cut into `world` blocks, each loaded as a shard on `device`."""
+    lib = _lib.load_library()
+    out = []
+    eo = np.ascontiguousarray(h.edge_offsets, dtype=np.uint64)
+    pins = np.ascontiguousarray(h.edge_members, dtype=np.uint32)
+    base = np.ascontiguousarray(h.base_weights, dtype=np.float64)
+    for r in range(world):
+        b, k = shard_bounds(h.num_edges, world, r)
+        if not k:
             continue
-        g = DeviceHypergraph.generate(family, edge_begin=b, m_local=k, device=device, **spec)
-        kappa += int(g.info().num_pins)
-        engines.append(LibEngine(g, shared))
-    return ShardedMatcher(engines, m, kappa, Collectives())
+        off = np.ascontiguousarray(eo[b:b + k + 1] - eo[b])
+        rows = pins[int(eo[b]):int(eo[b + k])]
+        view = _lib.CsrView(h.num_vertices, k, None, None, off.ctypes.data, rows.ctypes.data if rows.size else None,
+                            base[b:b + k].ctypes.data)
+        handle = C.c_void_p()
+        st = lib.hlm_b200_graph_upload_shard(C.byref(view), b, device, C.byref(handle))
+        if st != _lib.OK:
+            _raise(st, "hlm_b200_graph_upload_shard")
+        out.append(DeviceHypergraph(handle.value))
+    return out
 
 
 def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
-    """bench.py --gpus N (N > 1): config 5 shape, weak scaling -- every rank owns 250 M edges of an
-    8-uniform instance with n = 125 M * N vertices (N = 8 is BASELINE config 5 exactly)."""
+    """bench.py --gpus N (N > 1, or HLM_BENCH_FORCE_MG=1 on one GPU): config 5 shape, weak scaling -- every
+    rank owns 250 M edges of an 8-uniform instance with n = 125 M * N vertices (N = 8 is BASELINE config 5
+    exactly).  One call of hlm_b200_match_sharded per step."""
     import torch
 
     per_rank_m = int(os.environ.get("HLM_BENCH_MG_EDGES", 250_000_000))
@@ -389,27 +192,28 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
     m, n, d = per_rank_m * world, per_rank_n * world, 8
     b, k = shard_bounds(m, world, rank)
     g = DeviceHypergraph.generate("uniform", n=n, m=m, d=d, seed=1, edge_begin=b, m_local=k, device=local_rank)
-    eng = LibEngine(g)
-    coll = Collectives(dist)
-    sm = ShardedMatcher([eng], m, m * d, coll)
+    comm = Communicator.from_torch(dist, local_rank)
+    tstream = torch.cuda.Stream()
+    g.set_stream(tstream.cuda_stream)
     stream = WeightStream()
-    cfg = ParallelConfig(variant="crcw")
+    cfg = ParallelConfig()
     extras = extras or {}
     sampler = extras.get("sampler")
     if sampler:
         sampler.start()  # before the warm-up: nvidia-smi needs a moment before its first line
     for _ in range(max(3, args.warmup)):
-        res = sm.match(stream, cfg, gather=False)
+        res, rep = match_sharded([g], stream, cfg, comm)
     dist.barrier()
     torch.cuda.synchronize()
     if sampler:
         sampler.begin()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(eng.stream):
-        ev0.record(eng.stream)
-        for _ in range(args.steps):
-            res = sm.match(stream, cfg, gather=False)
-        ev1.record(eng.stream)
+    launches = 0
+    ev0.record(tstream)
+    for _ in range(args.steps):
+        res, rep = match_sharded([g], stream, cfg, comm)
+        launches += rep["kernel_launches"]
+    ev1.record(tstream)
     torch.cuda.synchronize()
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -425,11 +229,10 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
                                                             res.report.deactivated_per_round)
             achieved = total_bytes / (total_ms / args.steps * 1e-3) / 1e9
             peak = extras["hbm_gbs"] * world
-            roofline = {"bound": "hbm", "kernel": "whole job (round sweeps + checks + collectives), all ranks",
+            roofline = {"bound": "hbm", "kernel": "whole job (vertex-owned sweeps + candidate checks + collectives), all ranks",
                         "achieved": achieved, "peak": peak, "peak_source": extras["peak_src"] + f" x {world} GPUs",
                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                        "collective_ms_per_step": sm.timings.get("collective_ms"),
-                        "collective_bytes_per_step": sm.timings.get("collective_bytes")}
+                        "algorithmic_bytes": total_bytes}
         line = {"metric": "pins_per_sec_to_maximal_matching", "value": value, "unit": "pins/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -437,16 +240,23 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
                 "config": {"workload": f"config 5 shape: 8-uniform, n={n}, m={m} edge-partitioned over {world} GPUs "
                                        f"({per_rank_m} edges per GPU), unit weights, default stream",
                            "pins": m * d, "rounds": res.report.rounds, "matched": int(sum(res.report.matched_per_round_count)),
-                           "collectives_per_round": "all-reduce(max) int64[n] + all-reduce(sum) int32[n/2] + int32[n/8]",
-                           "collective_ms_last_step": sm.timings.get("collective_ms"),
+                           "driver": "hlm_b200_match_sharded (C++ round loop, NCCL %d bound by dlopen)" % comm.nccl_version(),
+                           "collectives_per_round": "all-reduce(max) uint64[live vertices] + all-reduce(sum) uint32[n/32 + 8] "
+                                                    "+ all-reduce(sum) uint32[4]",
+                           "collective_bytes_per_round": rep["collective_bytes_per_round"],
+                           "live_vertices_per_round": rep["live_vertices_per_round"],
+                           "host_syncs_per_step": rep["host_syncs"], "nccl_calls_per_step": rep["nccl_calls"],
                            "l2_policy": "inputs larger than L2; no flush"},
-                "gpu_launches": int(res.report.kernel_launches) * args.steps,
+                "gpu_launches": int(launches),
                 "clocks": clocks, "roofline": roofline,
                 "cpu_baseline": {"value": None, "unit": "pins/s", "cores": 0, "kind": "unavailable",
                                  "sample": "N > 1: the CPU baseline is reported by the N = 1 run (config 5 does not "
                                            "fit host memory)"},
-                "e2e": {"value": value, "unit": "pins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                        "note": "instance generated on the devices (16 G pins do not fit host memory)"}}
+                "e2e": {"value": value, "unit": "pins/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": int(res.matching.matched_edges.nbytes * 1.5),
+                        "note": "instance generated on the devices (16 G pins do not fit host memory); the result "
+                                "slices are copied to the host inside the timed region"}}
         emit = extras.get("emit") or (lambda text: print(text, flush=True))
         emit(json.dumps(line))
     dist.barrier()
+    comm.destroy()

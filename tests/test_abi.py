@@ -26,7 +26,7 @@ def test_header_symbols_are_exported(hb):
         assert hasattr(lib, name), f"{name} declared in include/hlm_b200.h but not exported"
     # the Python binding covers the same set
     assert sorted(_lib.SYMBOLS) == declared
-    assert lib.hlm_b200_abi_version() == 2
+    assert lib.hlm_b200_abi_version() == 3
 
 
 def test_struct_layouts_match_the_header(hb, tmp_path):
@@ -36,13 +36,14 @@ def test_struct_layouts_match_the_header(hb, tmp_path):
     from paper_2602_22976_b200 import _lib
 
     src = tmp_path / "sizes.c"
-    src.write_text('#include <stdio.h>\n#include "hlm_b200.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu\\n",'
+    src.write_text('#include <stdio.h>\n#include "hlm_b200.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n",'
                    "sizeof(hlm_b200_csr_view),sizeof(hlm_b200_stream),sizeof(hlm_b200_config),"
-                   "sizeof(hlm_b200_syn_spec),sizeof(hlm_b200_graph_info),sizeof(hlm_b200_result));return 0;}\n")
+                   "sizeof(hlm_b200_syn_spec),sizeof(hlm_b200_graph_info),sizeof(hlm_b200_result),"
+                   "sizeof(hlm_b200_shard_report));return 0;}\n")
     exe = tmp_path / "sizes"
     subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     sizes = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
-    mirrors = [_lib.CsrView, _lib.Stream, _lib.Config, _lib.SynSpec, _lib.GraphInfo, _lib.Result]
+    mirrors = [_lib.CsrView, _lib.Stream, _lib.Config, _lib.SynSpec, _lib.GraphInfo, _lib.Result, _lib.ShardReport]
     assert sizes == [ctypes.sizeof(m) for m in mirrors]
 
 
