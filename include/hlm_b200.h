@@ -124,7 +124,9 @@ typedef struct {
   uint32_t graph_launches;         /* CUDA-graph launches (each runs many rounds) */
   uint32_t write_conflicts;        /* always 0 (RunReport::write_conflicts) */
   /* HLM_B200_FLAG_KERNEL_TIMES: rounds + 1 entries each (the last filter launch finds the empty
-   * list); NULL otherwise.  filter = k_filter_vmax (all classes), check = k_check_commit. */
+   * list); NULL otherwise.  CRCW engine: filter = the round sweep (invalidate + compact + vertex-max, all
+   * classes), check = k_check_commit.  Vertex-owned engine: filter = the vertex-max sweep (k_c2_argmax_*),
+   * check = agreement + deactivation (k_c2_check, k_c2_kill_*, k_c2_count_alive). */
   float* round_filter_ms;
   float* round_check_ms;
   uint64_t h2d_bytes;              /* hlm_b200_match_host: bytes the loader moved host -> device */
@@ -267,6 +269,14 @@ enum { HLM_B200_DEGREE_ZERO_REJECT = 0, HLM_B200_DEGREE_ZERO_DROP = 1 };
 int hlm_b200_parse_hgr(const char* text, size_t len, int degree_zero, hlm_b200_host_graph* out);
 int hlm_b200_parse_metis_graph(const char* text, size_t len, int degree_zero, hlm_b200_host_graph* out);
 void hlm_b200_host_graph_free(hlm_b200_host_graph* g);
+/* Instance generators of the reference (generators.hpp), host only, bit-identical output:
+ * generate_random (:65-93; BASELINE config 1 = {1000000, 1000000, 4, 4, seed 1}), generate_tight_family
+ * (:37-54) and random_weights_1_100 (:96-101; `out` holds num_edges doubles).  Release the graphs with
+ * hlm_b200_host_graph_free.  Bad parameters are HLM_B200_ERR_INPUT with the reference's messages. */
+int hlm_b200_generate_random(uint32_t num_vertices, uint32_t num_edges, uint32_t min_edge_size, uint32_t max_edge_size,
+                             uint64_t seed, hlm_b200_host_graph* out);
+int hlm_b200_generate_tight_family(uint32_t d, double epsilon, hlm_b200_host_graph* out);
+int hlm_b200_random_weights_1_100(uint32_t num_edges, uint64_t seed, double* out);
 /* *text is NUL-terminated, *len excludes the NUL; release with hlm_b200_text_free */
 int hlm_b200_write_hgr(const hlm_b200_csr_view* h, char** text, size_t* len);
 int hlm_b200_write_matching(const uint32_t* matched, uint64_t count, double total_weight, uint32_t rounds,

@@ -157,6 +157,40 @@ inline Matching greedy_sorted(const Hypergraph& h) {
   return ::hlm::b200::run_variant(h, WeightStream{}, cfg, 0).matching;
 }
 
+namespace detail {
+inline Hypergraph take_host_graph(hlm_b200_host_graph& g) {
+  Hypergraph h;
+  const std::uint64_t kappa = g.num_edges ? g.edge_offsets[g.num_edges] : 0;
+  h.num_vertices = g.num_vertices;
+  h.num_edges = g.num_edges;
+  h.vertex_offsets.assign(g.vertex_offsets, g.vertex_offsets + g.num_vertices + 1);
+  h.vertex_incidence.assign(g.vertex_incidence, g.vertex_incidence + kappa);
+  h.edge_offsets.assign(g.edge_offsets, g.edge_offsets + g.num_edges + 1);
+  h.edge_members.assign(g.edge_members, g.edge_members + kappa);
+  h.base_weights.assign(g.base_weights, g.base_weights + g.num_edges);
+  hlm_b200_host_graph_free(&g);
+  return h;
+}
+}  // namespace detail
+
+// generate_random / random_weights_1_100 (generators.hpp:65-101) through the library's host code
+#ifndef HLM_B200_NO_REFERENCE_HEADERS
+inline Hypergraph generate_random(const RandomInstanceSpec& spec) {
+  hlm_b200_host_graph g;
+  const int st = hlm_b200_generate_random(spec.num_vertices, spec.num_edges, spec.min_edge_size, spec.max_edge_size,
+                                          spec.seed, &g);
+  if (st == HLM_B200_ERR_INPUT) throw input_error(hlm_b200_last_error());
+  if (st != HLM_B200_OK) throw std::runtime_error(std::string("hlm_b200: ") + hlm_b200_last_error());
+  return detail::take_host_graph(g);
+}
+#endif
+
+inline std::vector<double> random_weights_1_100(std::uint32_t num_edges, std::uint64_t seed) {
+  std::vector<double> w(num_edges);
+  hlm_b200_random_weights_1_100(num_edges, seed, w.data());
+  return w;
+}
+
 // compact (local_max_par.hpp:350-454) on the device
 inline CompactResult compact(const Hypergraph& h, std::span<const std::uint8_t> vertex_active,
                              std::span<const std::uint8_t> edge_active, unsigned /*workers*/ = 1,

@@ -10,6 +10,9 @@
  * File:line citations are relative to /root/reference/proj/include/hlm/.
  */
 #define _POSIX_C_SOURCE 200809L
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include "hlm_oracle.h"
 
 #include <stdlib.h>
@@ -326,6 +329,44 @@ int orc_build_incidence(uint32_t n, uint32_t m, const uint64_t* edge_offsets,
                         uint32_t* vertex_incidence) {
   const uint64_t kappa = m ? edge_offsets[m] : 0;
   memset(vertex_offsets, 0, sizeof(uint64_t) * ((size_t)n + 1));
+  /* Large instances (the full BASELINE configs for bench.py's reference arm): every thread owns a
+   * range of vertices and walks all pins, so counters and cursors are private to their owner and a
+   * list is filled in ascending edge order, exactly like the sequential form below. */
+  int bad = 0;
+#ifdef _OPENMP
+  if (kappa >= (1ull << 22)) {
+#pragma omp parallel
+    {
+      const uint32_t nt = (uint32_t)omp_get_num_threads(), t = (uint32_t)omp_get_thread_num();
+      const uint32_t lo = (uint32_t)((uint64_t)n * t / nt), hi = (uint32_t)((uint64_t)n * (t + 1) / nt);
+      for (uint64_t i = 0; i < kappa; ++i) {
+        const uint32_t v = edge_members[i];
+        if (v >= n) {
+          if (t == 0) bad = 1;
+        } else if (v >= lo && v < hi) {
+          ++vertex_offsets[v + 1];
+        }
+      }
+    }
+    if (bad) return ORC_INPUT_ERROR;
+    for (uint32_t v = 0; v < n; ++v) vertex_offsets[v + 1] += vertex_offsets[v];
+    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)n + 1));
+    if (!cur) return ORC_NOMEM;
+    memcpy(cur, vertex_offsets, sizeof(uint64_t) * (size_t)n);
+#pragma omp parallel
+    {
+      const uint32_t nt = (uint32_t)omp_get_num_threads(), t = (uint32_t)omp_get_thread_num();
+      const uint32_t lo = (uint32_t)((uint64_t)n * t / nt), hi = (uint32_t)((uint64_t)n * (t + 1) / nt);
+      for (uint32_t e = 0; e < m; ++e)
+        for (uint64_t i = edge_offsets[e]; i < edge_offsets[e + 1]; ++i) {
+          const uint32_t v = edge_members[i];
+          if (v >= lo && v < hi) vertex_incidence[cur[v]++] = e;
+        }
+    }
+    free(cur);
+    return ORC_OK;
+  }
+#endif
   for (uint64_t i = 0; i < kappa; ++i) {
     if (edge_members[i] >= n) return ORC_INPUT_ERROR;
     ++vertex_offsets[edge_members[i] + 1];
@@ -580,19 +621,31 @@ int orc_syn_generate(const orc_syn_spec* spec, orc_owned_graph* out) {
   if (spec->family == ORC_SYN_UNIFORM && (spec->d == 0 || spec->d > n)) return ORC_INPUT_ERROR;
   orc_syn_spec sp = *spec;
   sp.n = n;
+  /* counter-based: every edge is a pure function of (seed, e), so the rows are filled in parallel
+   * (OpenMP; the full BASELINE configs are generated on the host for the reference arm of bench.py) */
+  uint32_t* sizes = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)sp.m);
+  if (!sizes) return ORC_NOMEM;
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < (int64_t)sp.m; ++e) sizes[e] = orc_syn_edge_size(&sp, (uint32_t)e);
   uint64_t kappa = 0;
-  for (uint32_t e = 0; e < sp.m; ++e) kappa += orc_syn_edge_size(&sp, e);
+  for (uint32_t e = 0; e < sp.m; ++e) kappa += sizes[e];
   int rc = alloc_graph(out, n, sp.m, kappa);
-  if (rc != ORC_OK) return rc;
+  if (rc != ORC_OK) {
+    free(sizes);
+    return rc;
+  }
   uint64_t pos = 0;
   for (uint32_t e = 0; e < sp.m; ++e) {
-    const uint32_t s = orc_syn_edge_size(&sp, e);
     out->edge_offsets[e] = pos;
-    orc_syn_edge_pins(&sp, e, s, out->edge_members + pos);
-    out->base_weights[e] = orc_syn_weight(&sp, e);
-    pos += s;
+    pos += sizes[e];
   }
   out->edge_offsets[sp.m] = pos;
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t e = 0; e < (int64_t)sp.m; ++e) {
+    orc_syn_edge_pins(&sp, (uint32_t)e, sizes[e], out->edge_members + out->edge_offsets[e]);
+    out->base_weights[e] = orc_syn_weight(&sp, (uint32_t)e);
+  }
+  free(sizes);
   return orc_build_incidence(n, sp.m, out->edge_offsets, out->edge_members, out->vertex_offsets,
                              out->vertex_incidence);
 }

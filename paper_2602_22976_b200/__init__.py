@@ -23,12 +23,15 @@ from .api import (  # noqa: F401
     compact,
     default_max_rounds,
     eval_stream,
+    generate_random,
+    generate_tight_family,
     load_instance_file,
     local_max_crcw,
     local_max_crew,
     parse_hgr,
     parse_matching,
     parse_metis_graph,
+    random_weights_1_100,
     run_variant,
     verify_matching,
     write_hgr,

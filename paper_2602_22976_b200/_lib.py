@@ -106,6 +106,10 @@ SYMBOLS = {
     "hlm_b200_shard_report_free": (None, [C.POINTER(ShardReport)]),
     "hlm_b200_parse_hgr": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
     "hlm_b200_parse_metis_graph": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(HostGraph)]),
+    "hlm_b200_generate_random": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                           C.POINTER(HostGraph)]),
+    "hlm_b200_generate_tight_family": (C.c_int, [C.c_uint32, C.c_double, C.POINTER(HostGraph)]),
+    "hlm_b200_random_weights_1_100": (C.c_int, [C.c_uint32, C.c_uint64, C.c_void_p]),
     "hlm_b200_host_graph_free": (None, [C.POINTER(HostGraph)]),
     "hlm_b200_write_hgr": (C.c_int, [C.POINTER(CsrView), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "hlm_b200_write_matching": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, C.c_uint32, C.POINTER(C.c_void_p),

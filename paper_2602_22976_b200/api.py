@@ -432,6 +432,36 @@ def parse_metis_graph(text, degree_zero: str = "reject") -> Hypergraph:
     return _parse("hlm_b200_parse_metis_graph", text, degree_zero, None)
 
 
+def generate_random(num_vertices: int, num_edges: int, min_edge_size: int = 2, max_edge_size: int = 3,
+                    seed: int = 1) -> Hypergraph:
+    """generate_random (generators.hpp:65-93), RandomInstanceSpec's fields and defaults (:56-62)."""
+    hg = _lib.HostGraph()
+    st = _lib.load_library().hlm_b200_generate_random(num_vertices, num_edges, min_edge_size, max_edge_size,
+                                                      seed & 0xFFFFFFFFFFFFFFFF, C.byref(hg))
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_generate_random")
+    return _take_host_graph(hg)
+
+
+def generate_tight_family(d: int, epsilon: float) -> Hypergraph:
+    """generate_tight_family (generators.hpp:37-54)."""
+    hg = _lib.HostGraph()
+    st = _lib.load_library().hlm_b200_generate_tight_family(d, epsilon, C.byref(hg))
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_generate_tight_family")
+    return _take_host_graph(hg)
+
+
+def random_weights_1_100(num_edges: int, seed: int) -> np.ndarray:
+    """random_weights_1_100 (generators.hpp:96-101)."""
+    out = np.empty(num_edges, dtype=np.float64)
+    st = _lib.load_library().hlm_b200_random_weights_1_100(num_edges, seed & 0xFFFFFFFFFFFFFFFF,
+                                                           out.ctypes.data if num_edges else None)
+    if st != _lib.OK:
+        _raise(st, "hlm_b200_random_weights_1_100")
+    return out
+
+
 def _text_out(st: int, what: str, ptr: C.c_void_p, length: C.c_size_t) -> str:
     if st != _lib.OK:
         _raise(st, what)

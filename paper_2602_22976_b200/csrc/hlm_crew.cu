@@ -329,11 +329,8 @@ static int crew_setup(Graph* g) {
 
 static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out,
                            int report_variant) {
-  const uint32_t max_rounds = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
-  if (max_rounds > 65000u) {
-    set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
-    return HLM_B200_ERR_UNSUPPORTED;
-  }
+  const uint32_t requested = cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m);
+  const uint32_t max_rounds = std::min(requested, 65000u);  // 16-bit round record; see match_crcw
   ST_CHECK(ensure_workspace(g, max_rounds));
   ST_CHECK(crew_setup(g));
   Workspace& w = g->ws;
@@ -412,6 +409,10 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
   out->device_edge_visits = static_cast<uint64_t>(g->m) * round;
   int rc = assemble_result(g, round, cfg, report_variant, out);
   if (rc != HLM_B200_OK) return rc;
+  if (limit && requested > max_rounds) {
+    set_error("the run needs more than %u rounds (16-bit round record)", max_rounds);
+    return HLM_B200_ERR_UNSUPPORTED;
+  }
   return limit ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
 }
 

@@ -95,20 +95,24 @@ static int dev_alloc(T** p, size_t count, Graph* g) {
   return HLM_B200_OK;
 }
 
-static cudaStream_t g_alloc_stream[64] = {};
+// One allocation stream per device, created once (handles of different instances may be used from
+// different threads); devices beyond the table share the legacy stream, which is correct, only slower.
+constexpr int kMaxPoolDevices = 64;
+static cudaStream_t g_alloc_stream[kMaxPoolDevices] = {};
+static std::once_flag g_alloc_once[kMaxPoolDevices];
 
 static cudaStream_t alloc_stream() {
   int dev = 0;
   cudaGetDevice(&dev);
-  dev &= 63;
-  if (!g_alloc_stream[dev]) {
+  if (dev < 0 || dev >= kMaxPoolDevices) return nullptr;
+  std::call_once(g_alloc_once[dev], [dev] {
     cudaStreamCreateWithFlags(&g_alloc_stream[dev], cudaStreamNonBlocking);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       unsigned long long keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-  }
+  });
   return g_alloc_stream[dev];
 }
 
@@ -1083,11 +1087,14 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   // runs on the exact three-level path with a static key; the rounds it needs (the dependency
   // depth of the order) are an implementation detail, the reference reports one round.
   const bool greedy = cfg->variant == HLM_B200_VARIANT_GREEDY;
-  const uint32_t max_rounds = greedy ? 65000u : (cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m));
-  if (max_rounds > 65000u) {
-    set_error("max_rounds %u exceeds the 16-bit round record (65000)", max_rounds);
-    return HLM_B200_ERR_UNSUPPORTED;
-  }
+  // greedy: the rounds are an implementation detail; what is left after kGreedyRounds of them is
+  // finished by one ordered scan (hlm_greedy.cu), so the depth of the order never shows
+  uint32_t greedy_rounds = 64;
+  if (const char* genv = std::getenv("HLM_B200_GREEDY_ROUNDS")) greedy_rounds = std::max(1, std::atoi(genv));
+  const uint32_t requested = greedy ? greedy_rounds : (cfg->max_rounds ? cfg->max_rounds : default_max_rounds(g->m));
+  // the round record is 16 bits wide: a larger cap is honoured up to 65000 rounds (no instance comes
+  // near: the default cap is 64 + 4 log2 m), and only a run that really gets there is refused
+  const uint32_t max_rounds = std::min(requested, 65000u);
   cudaStream_t s = g->stream;
   PhaseTrace tr;
   ST_CHECK(ensure_workspace(g, max_rounds));
@@ -1223,11 +1230,18 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     }
   }
   tr.mark("match: rounds");
+  if (greedy && c.status == ST_ROUND_LIMIT) {
+    uint64_t finished = 0;
+    ST_CHECK(greedy_finish(g, rounds + 1u, &finished));
+    out->kernel_launches += 3;
+    c.status = ST_DONE;
+    tr.mark("match: greedy tail");
+  }
   int rc = assemble_result(g, rounds, cfg, cfg->variant, out);
   tr.mark("match: result");
   if (rc != HLM_B200_OK) return rc;
-  if (greedy && c.status == ST_ROUND_LIMIT) {
-    set_error("greedy: the dependency depth of the (weight, id) order exceeds %u rounds", max_rounds);
+  if (c.status == ST_ROUND_LIMIT && requested > max_rounds) {
+    set_error("the run needs more than %u rounds (16-bit round record)", max_rounds);
     return HLM_B200_ERR_UNSUPPORTED;
   }
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;

@@ -123,6 +123,8 @@ bool reorder_enabled();
 bool renumber_enabled();
 int reorder_by_first_pin(Graph* g);
 bool crcw_is_faster(const Graph* g);
+// the rest of greedy_sorted as one ordered scan over the still-free edges (hlm_greedy.cu)
+int greedy_finish(Graph* g, uint32_t round, uint64_t* finished);
 int renumber_by_degree(Graph* g);
 int build_base_codes(Graph* g);
 int download_pins_original_order(Graph* g, const uint32_t* resident_pins, uint32_t* host_pins);

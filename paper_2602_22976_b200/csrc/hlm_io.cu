@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 #include <string>
 #include <string_view>
 #include <vector>
@@ -67,21 +68,32 @@ void split_tokens(std::string_view line, std::vector<std::string_view>& tokens) 
   }
 }
 
-uint64_t parse_uint(std::string_view tok, const char* what) {  // io.hpp:49-56
-  uint64_t value = 0;
-  auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), value);
-  if (ec != std::errc{} || ptr != tok.data() + tok.size())
-    throw ParseError{std::string("expected unsigned integer for ") + what + ", got '" + std::string(tok) + "'"};
-  return value;
+// A token is a number only if ALL of it is (what io.hpp:49-66 accept and reject, messages included).
+uint64_t parse_uint(std::string_view tok, const char* what) {
+  uint64_t acc = 0;
+  bool good = !tok.empty();
+  for (size_t i = 0; good && i < tok.size(); ++i) {
+    const unsigned digit = static_cast<unsigned char>(tok[i]) - '0';
+    good = digit <= 9 && acc <= (UINT64_MAX - digit) / 10;  // no sign, no blanks, no wrap-around
+    if (good) acc = acc * 10 + digit;
+  }
+  if (!good) throw ParseError{std::string("expected unsigned integer for ") + what + ", got '" + std::string(tok) + "'"};
+  return acc;
 }
 
-double parse_weight(std::string_view tok) {  // io.hpp:58-66
-  double value = 0.0;
-  auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), value);
-  if (ec != std::errc{} || ptr != tok.data() + tok.size() || !std::isfinite(value))
-    throw ParseError{"malformed edge weight '" + std::string(tok) + "'"};
-  if (!(value > 0.0)) throw ParseError{"edge weight must be positive, got " + std::string(tok)};
-  return value;
+double parse_weight(std::string_view tok) {
+  double w = 0.0;
+  const char* last = tok.data() + tok.size();
+  const std::from_chars_result got = std::from_chars(tok.data(), last, w);  // locale-free, integers stay exact
+  const bool whole = got.ec == std::errc{} && got.ptr == last;
+  if (!whole || !std::isfinite(w)) throw ParseError{"malformed edge weight '" + std::string(tok) + "'"};
+  if (w <= 0.0) throw ParseError{"edge weight must be positive, got " + std::string(tok)};
+  return w;
+}
+
+// ids are 32-bit on both sides of the boundary: larger header counts are input errors, not narrowed
+void check_count(uint64_t value, const char* what) {
+  if (value > 0xFFFFFFFFull) throw ParseError{std::string(what) + " " + std::to_string(value) + " exceeds the 32-bit id range"};
 }
 
 struct EdgeLists {  // flat edge lists in file order
@@ -161,6 +173,8 @@ void parse_hgr(const char* text, size_t len, int degree_zero, hlm_b200_host_grap
   if (tok.size() < 2 || tok.size() > 3) throw ParseError{"malformed hgr header '" + std::string(line) + "'"};
   const uint64_t m = parse_uint(tok[0], "edge count");
   const uint64_t n = parse_uint(tok[1], "vertex count");
+  check_count(m, "edge count");
+  check_count(n, "vertex count");
   const uint64_t fmt = tok.size() == 3 ? parse_uint(tok[2], "fmt code") : 0;
   if (fmt != 0 && fmt != 1 && fmt != 10 && fmt != 11) throw ParseError{"unsupported hgr fmt code " + std::to_string(fmt)};
   const bool edge_w = fmt == 1 || fmt == 11, vertex_w = fmt == 10 || fmt == 11;
@@ -203,6 +217,8 @@ void parse_metis(const char* text, size_t len, int degree_zero, hlm_b200_host_gr
   if (tok.size() < 2 || tok.size() > 3) throw ParseError{"malformed graph header '" + std::string(line) + "'"};
   const uint64_t n = parse_uint(tok[0], "vertex count");
   const uint64_t m = parse_uint(tok[1], "edge count");
+  check_count(n, "vertex count");
+  check_count(m, "edge count");
   if (tok.size() == 3 && parse_uint(tok[2], "fmt code") != 0) throw ParseError{"weighted graph fmt codes are not supported"};
   std::vector<std::vector<uint32_t>> adj(n);
   for (uint64_t u = 0; u < n;) {
@@ -261,7 +277,70 @@ int guarded(F&& f) {
   } catch (const std::bad_alloc&) {
     set_error("out of host memory");
     return HLM_B200_ERR_NOMEM;
+  } catch (const std::length_error& e) {  // a header count no container can hold
+    set_error("instance too large: %s", e.what());
+    return HLM_B200_ERR_INPUT;
+  } catch (const std::exception& e) {  // nothing may cross the extern "C" boundary
+    set_error("%s", e.what());
+    return HLM_B200_ERR_INPUT;
+  } catch (...) {
+    set_error("unknown failure");
+    return HLM_B200_ERR_INPUT;
   }
+}
+
+// SplitMix64 as the reference's instance generators use it (generators.hpp:19-30)
+struct SeqRng {
+  uint64_t state;
+  uint64_t next() {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+};
+
+// generate_random (generators.hpp:65-93): per edge one size draw (consumed even when the span is 1), then
+// vertex draws until `size` distinct ones; unused vertices are dropped and the rest renumbered.
+void generate_random(uint32_t n, uint32_t m, uint32_t smin, uint32_t smax, uint64_t seed, hlm_b200_host_graph* out) {
+  if (n == 0 || m == 0) throw ParseError{"random instance needs at least one vertex and one edge"};
+  if (smin == 0 || smin > smax) throw ParseError{"random instance needs 1 <= min_edge_size <= max_edge_size"};
+  if (smax > n) throw ParseError{"edge size " + std::to_string(smax) + " exceeds vertex count " + std::to_string(n)};
+  SeqRng rng{seed};
+  const uint32_t span = smax - smin + 1;
+  EdgeLists el;
+  el.off.reserve(static_cast<size_t>(m) + 1);
+  el.pins.reserve(static_cast<size_t>(m) * ((smin + smax + 1) / 2));
+  for (uint32_t e = 0; e < m; ++e) {
+    const uint32_t size = smin + static_cast<uint32_t>(rng.next() % span);
+    const size_t first = el.pins.size();
+    while (el.pins.size() - first < size) {
+      const uint32_t v = static_cast<uint32_t>(rng.next() % n);
+      bool seen = false;
+      for (size_t i = first; i < el.pins.size(); ++i) seen |= el.pins[i] == v;
+      if (!seen) el.pins.push_back(v);
+    }
+    el.off.push_back(el.pins.size());
+  }
+  build(el, n, HLM_B200_DEGREE_ZERO_DROP, out);
+}
+
+// generate_tight_family (generators.hpp:37-54): d pair edges of weight 1, their left ends joined by one
+// rank-d edge of weight 1 + epsilon
+void generate_tight_family(uint32_t d, double epsilon, hlm_b200_host_graph* out) {
+  if (d < 2) throw ParseError{"tight family needs d >= 2"};
+  if (!(epsilon > 0.0)) throw ParseError{"tight family needs epsilon > 0"};
+  EdgeLists el;
+  for (uint32_t i = 0; i < d; ++i) {
+    el.pins.push_back(i);
+    el.pins.push_back(d + i);
+    el.off.push_back(el.pins.size());
+    el.weights.push_back(1.0);
+  }
+  for (uint32_t i = 0; i < d; ++i) el.pins.push_back(i);
+  el.off.push_back(el.pins.size());
+  el.weights.push_back(1.0 + epsilon);
+  build(el, 2 * d, HLM_B200_DEGREE_ZERO_REJECT, out);
 }
 
 }  // namespace
@@ -285,6 +364,33 @@ int hlm_b200_parse_metis_graph(const char* text, size_t len, int degree_zero, hl
   const int rc = guarded([&] { parse_metis(text, len, degree_zero, out); });
   if (rc != HLM_B200_OK) hlm_b200_host_graph_free(out);
   return rc;
+}
+
+int hlm_b200_generate_random(uint32_t num_vertices, uint32_t num_edges, uint32_t min_edge_size, uint32_t max_edge_size,
+                             uint64_t seed, hlm_b200_host_graph* out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  std::memset(out, 0, sizeof(*out));
+  const int rc = guarded([&] { generate_random(num_vertices, num_edges, min_edge_size, max_edge_size, seed, out); });
+  if (rc != HLM_B200_OK) hlm_b200_host_graph_free(out);
+  return rc;
+}
+
+int hlm_b200_generate_tight_family(uint32_t d, double epsilon, hlm_b200_host_graph* out) {
+  if (!out) return HLM_B200_ERR_INPUT;
+  std::memset(out, 0, sizeof(*out));
+  const int rc = guarded([&] { generate_tight_family(d, epsilon, out); });
+  if (rc != HLM_B200_OK) hlm_b200_host_graph_free(out);
+  return rc;
+}
+
+int hlm_b200_random_weights_1_100(uint32_t num_edges, uint64_t seed, double* out) {  // generators.hpp:96-101
+  if (!out && num_edges) {
+    set_error("null argument");
+    return HLM_B200_ERR_INPUT;
+  }
+  SeqRng rng{seed ^ 0x517CC1B727220A95ull};
+  for (uint32_t e = 0; e < num_edges; ++e) out[e] = static_cast<double>(1 + rng.next() % 100);
+  return HLM_B200_OK;
 }
 
 void hlm_b200_host_graph_free(hlm_b200_host_graph* g) {

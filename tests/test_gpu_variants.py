@@ -80,6 +80,16 @@ def test_greedy_variant_equals_greedy_sorted(hb, port, ref):
     cases.append(("three weight classes", g))
     g = po.graph_from_edge_lists([[i, i + 1] for i in range(300)])  # unit path: dependency depth 150
     cases.append(("unit path", g))
+    # long dependency chains: after 64 rounds the rest is finished by the ordered scan (hlm_greedy.cu)
+    g = po.graph_from_edge_lists([[i, i + 1] for i in range(20000)])
+    cases.append(("long unit path", g))
+    side = 120  # unit-weight mesh in natural order (what a METIS grid graph looks like)
+    mesh = [[r * side + c, r * side + c + 1] for r in range(side) for c in range(side - 1)]
+    mesh += [[r * side + c, (r + 1) * side + c] for r in range(side - 1) for c in range(side)]
+    cases.append(("unit mesh", po.graph_from_edge_lists(mesh)))
+    g = po.graph_from_edge_lists([[i, i + 1, i + 2] for i in range(15000)])
+    g.base_weights = (np.arange(g.m)[::-1] % 7 + 1).astype(np.float64) * 0.5  # weight classes along a 3-uniform chain
+    cases.append(("weighted 3-uniform chain", g))
     for name, g in cases:
         want = ref.local_max(g, po.Stream(), variant=po.VARIANT_GREEDY)
         got = hb.run_variant(to_hb_graph(g), hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
@@ -92,6 +102,16 @@ def test_greedy_variant_equals_greedy_sorted(hb, port, ref):
             assert_same_result(again, want, f"greedy resident {name}")
             v = dg.verify(again.matching.matched_edges)
             assert v.disjoint and v.maximal
+
+
+def test_a_generous_round_cap_is_accepted(hb, port):
+    """The reference takes any uint32 max_rounds; a cap used as "unlimited" must run, not be refused."""
+    g = port.generate_random(2000, 4000, 2, 4, 5)
+    s = po.Stream(seed=3)
+    want = port.local_max(g, s)
+    for variant in ("crcw", "crew", "auto"):
+        got = hb.run_variant(to_hb_graph(g), to_hb_stream(s), hb.ParallelConfig(variant=variant, max_rounds=1_000_000))
+        assert_same_result(got, want, f"max_rounds 1e6 {variant}")
 
 
 def test_quality_band_vs_greedy_acceptance_criterion_7(hb, port):
