@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -479,6 +480,128 @@ struct HostScan {
     }
   }
   bool weights_ready() const { return weight_chunks_done.load(std::memory_order_acquire) == chunks_per_array(); }
+  // one chunk of the queue above; false once the queue is empty
+  bool step() {
+    const uint64_t nc = chunks_per_array();
+    const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
+    if (t >= 2 * nc) return false;
+    const bool is_off = t >= nc;
+    const uint64_t b = (is_off ? t - nc : t) * kChunk, e = std::min(m, b + kChunk);
+    if (is_off) {
+      if (!nonuniform.load(std::memory_order_relaxed) && host_offsets_differ(off, d0, b, e))
+        nonuniform.store(true, std::memory_order_relaxed);
+    } else {
+      if (!nopack.load(std::memory_order_relaxed) && host_pack_weights_u8(w, packed, b, e))
+        nopack.store(true, std::memory_order_relaxed);
+      weight_chunks_done.fetch_add(1, std::memory_order_release);
+    }
+    return true;
+  }
+};
+
+// Pageable caller memory (std::vector storage: what the reference's Hypergraph hands over).  A plain
+// cudaMemcpyAsync from it is staged by the driver through one small bounce buffer at a fraction of the
+// PCIe rate (measured on config 2: 226 ms for the call against 56 ms from page-locked arrays).  Here the
+// host threads that already scan / pack do the staging themselves: they copy 8 MB chunks of the pin
+// array into a ring of page-locked slots, the coordinating thread issues one DMA per filled chunk in
+// order and frees a slot when its DMA has completed.  The ring lives for the process.
+struct PinStager {
+  static constexpr size_t kMaxSlots = 64;
+  static constexpr size_t kRingBytes = 256u << 20;
+  // chunk size / slots in use (HLM_B200_STAGE_CHUNK_KB / HLM_B200_STAGE_SLOTS): a ring that stays in the
+  // host's last-level cache keeps the staging writes and the DMA reads out of DRAM
+  // (config 2, 16-core host with 60 MB of L3: 8 MB x 24 slots 111 ms per call, 2 MB x 24 76, 4 MB x 48 84,
+  // 4 MB x 8 71; from page-locked arrays 56.5)
+  size_t kChunkBytes = 4u << 20;
+  size_t kSlots = 8;
+  const char* src = nullptr;
+  char* dst = nullptr;  // device
+  size_t bytes = 0, chunks = 0;
+  char* ring = nullptr;
+  std::atomic<size_t> next{0};    // next chunk a worker may fill
+  std::atomic<size_t> freed{0};   // chunks whose DMA completed: chunk c may be filled once c < freed + kSlots
+  std::unique_ptr<std::atomic<uint8_t>[]> filled;
+  size_t issued = 0;
+  cudaEvent_t ev[kMaxSlots] = {};
+  bool active = false;
+
+  static char* ring_memory() {
+    static char* mem = [] {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, kRingBytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+      }
+      return static_cast<char*>(p);
+    }();
+    return mem;
+  }
+  static bool pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+  }
+  bool init(const void* from, void* to, size_t n) {
+    ring = ring_memory();
+    if (!ring) return false;
+    if (const char* cenv = std::getenv("HLM_B200_STAGE_CHUNK_KB")) kChunkBytes = std::max<size_t>(64, std::strtoull(cenv, nullptr, 10)) << 10;
+    if (const char* senv = std::getenv("HLM_B200_STAGE_SLOTS")) kSlots = std::strtoull(senv, nullptr, 10);
+    kChunkBytes = std::min(kChunkBytes, kRingBytes / 2) & ~static_cast<size_t>(63);
+    kSlots = std::max<size_t>(2, std::min(std::min(kSlots, kMaxSlots), kRingBytes / kChunkBytes));
+    for (size_t i = 0; i < kSlots; ++i)
+      if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) return false;
+    src = static_cast<const char*>(from);
+    dst = static_cast<char*>(to);
+    bytes = n;
+    chunks = (n + kChunkBytes - 1) / kChunkBytes;
+    filled.reset(new std::atomic<uint8_t>[chunks]);
+    for (size_t c = 0; c < chunks; ++c) filled[c].store(0, std::memory_order_relaxed);
+    active = true;
+    return true;
+  }
+  ~PinStager() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  // worker side: fill one chunk if a slot is free.  0 = nothing left, 1 = filled one, 2 = ring full
+  int fill_one() {
+    for (;;) {
+      size_t c = next.load(std::memory_order_relaxed);
+      if (c >= chunks) return 0;
+      if (c >= freed.load(std::memory_order_acquire) + kSlots) return 2;
+      if (!next.compare_exchange_weak(c, c + 1, std::memory_order_relaxed)) continue;
+      const size_t at = c * kChunkBytes, len = std::min(kChunkBytes, bytes - at);
+      std::memcpy(ring + (c % kSlots) * kChunkBytes, src + at, len);
+      filled[c].store(1, std::memory_order_release);
+      return 1;
+    }
+  }
+  // coordinator side: DMAs for the chunks filled so far (in order), slots of completed DMAs back to the ring.
+  // after_chunk(c): called when chunk c has been queued on `s`
+  template <typename F>
+  cudaError_t pump(cudaStream_t s, F&& after_chunk) {
+    while (issued < chunks && filled[issued].load(std::memory_order_acquire)) {
+      const size_t at = issued * kChunkBytes, len = std::min(kChunkBytes, bytes - at);
+      cudaError_t e = cudaMemcpyAsync(dst + at, ring + (issued % kSlots) * kChunkBytes, len, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[issued % kSlots], s);
+      if (e != cudaSuccess) return e;
+      after_chunk(issued);
+      ++issued;
+    }
+    size_t f = freed.load(std::memory_order_relaxed);
+    while (f < issued) {
+      const cudaError_t q = cudaEventQuery(ev[f % kSlots]);
+      if (q == cudaErrorNotReady) break;
+      if (q != cudaSuccess) return q;
+      ++f;
+    }
+    freed.store(f, std::memory_order_release);
+    return cudaSuccess;
+  }
+  bool all_issued() const { return issued == chunks; }
 };
 
 static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const UploadPlan& plan = UploadPlan()) {
@@ -528,8 +651,6 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     scan.packed = static_cast<uint8_t*>(host_result_alloc(m));
     if (!scan.packed) scan.nopack = true;
     if (scan.d0 == 0 || scan.d0 > kLargeEdge) scan.nonuniform = true;  // plain path handles these
-    const unsigned nt = std::min(hc, 32u);
-    for (unsigned t = 0; t + 1 < nt; ++t) workers.emplace_back([&scan] { scan.work([] {}); });
   }
   cudaError_t e = cudaSuccess;
   // The pins go up in 256 MB pieces; a second stream takes the largest vertex id of every piece
@@ -549,19 +670,34 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   } side;
   bool pins_checked = false;
   const EdgeStats st_init = {0xffffffffu, 0, 0, 0, 0, 0};
+  PinStager stager;
+  uint64_t piece = 64ull << 20;  // entries: 256 MB
+  if (const char* penv = std::getenv("HLM_B200_PIN_PIECE_MB")) piece = std::max<uint64_t>(1, std::strtoull(penv, nullptr, 10)) << 18;
+  // after `done` entries of the pin array are on their way: validate the finished 256 MB pieces on the side stream
+  uint64_t checked_upto = 0;
+  auto side_check_upto = [&](uint64_t done) {
+    while (e == cudaSuccess && checked_upto < done && (done - checked_upto >= piece || done == g->kappa)) {
+      const uint64_t len = std::min(piece, done - checked_upto);
+      e = cudaEventRecord(side.ev, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side.s2, side.ev, 0);
+      if (e == cudaSuccess) k_max_pin<<<grid_for(g, len), kBlock, 0, side.s2>>>(g->pins + checked_upto, len, side.d_st);
+      checked_upto += len;
+    }
+  };
   if (g->kappa) {
     if (assist && dev_alloc(&side.d_st, 1, nullptr) == HLM_B200_OK &&
         cudaStreamCreateWithFlags(&side.s2, cudaStreamNonBlocking) == cudaSuccess &&
         cudaEventCreateWithFlags(&side.ev, cudaEventDisableTiming) == cudaSuccess) {
       e = cudaMemcpyAsync(side.d_st, &st_init, sizeof(st_init), cudaMemcpyHostToDevice, side.s2);
-      uint64_t piece = 64ull << 20;  // entries: 256 MB
-      if (const char* penv = std::getenv("HLM_B200_PIN_PIECE_MB")) piece = std::max<uint64_t>(1, std::strtoull(penv, nullptr, 10)) << 18;
-      for (uint64_t at = 0; at < g->kappa && e == cudaSuccess; at += piece) {
-        const uint64_t len = std::min(piece, g->kappa - at);
-        e = cudaMemcpyAsync(g->pins + at, h->edge_members + at, len * 4, cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaEventRecord(side.ev, s);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(side.s2, side.ev, 0);
-        if (e == cudaSuccess) k_max_pin<<<grid_for(g, len), kBlock, 0, side.s2>>>(g->pins + at, len, side.d_st);
+      const bool stage = e == cudaSuccess && !std::getenv("HLM_B200_NO_STAGING") && g->kappa * 4 >= (64ull << 20) &&
+                         PinStager::pageable(h->edge_members) && stager.init(h->edge_members, g->pins, g->kappa * 4);
+      if (!stage) {
+        // page-locked caller memory: the DMA reads it in place, in 256 MB pieces
+        for (uint64_t at = 0; at < g->kappa && e == cudaSuccess; at += piece) {
+          const uint64_t len = std::min(piece, g->kappa - at);
+          e = cudaMemcpyAsync(g->pins + at, h->edge_members + at, len * 4, cudaMemcpyHostToDevice, s);
+          side_check_upto(at + len);
+        }
       }
       pins_checked = e == cudaSuccess;
     } else {
@@ -599,7 +735,41 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   };
   rc = HLM_B200_OK;
   if (assist) {
-    scan.work(queue_weights);  // this thread helps once the copy is queued
+    // workers: stage pin chunks while the ring has room (PCIe is the longest pole: keep it fed), scan /
+    // pack otherwise
+    const unsigned nt = std::min(hc, 32u);
+    for (unsigned t = 0; t + 1 < nt; ++t)
+      workers.emplace_back([&scan, &stager] {
+        bool more_scan = true;
+        for (;;) {
+          const int f = stager.active ? stager.fill_one() : 0;
+          if (f == 1) continue;
+          if (more_scan && (more_scan = scan.step())) continue;
+          if (f == 0) break;
+          std::this_thread::yield();  // ring full and nothing else to do
+        }
+      });
+    // this thread: issues the DMAs of the staged chunks, queues the packed weights once they are complete,
+    // and helps with the scan in between
+    bool more_scan = true;
+    const uint64_t per_chunk = stager.kChunkBytes / 4;
+    for (;;) {
+      if (stager.active && e == cudaSuccess) {
+        const cudaError_t pe = stager.pump(s, [&](size_t c) { side_check_upto(std::min<uint64_t>(g->kappa, (c + 1) * per_chunk)); });
+        if (pe != cudaSuccess) e = pe;
+      }
+      queue_weights();
+      const bool pins_done = !stager.active || stager.all_issued() || e != cudaSuccess;
+      if (more_scan && pins_done) {  // never while DMAs wait to be issued: a scan chunk takes ~1 ms, a DMA 0.15 ms
+        more_scan = scan.step();
+        continue;
+      }
+      if (pins_done && !more_scan) break;
+      std::this_thread::yield();
+    }
+    if (e != cudaSuccess && stager.active) {  // let the workers run out
+      stager.freed.store(stager.chunks, std::memory_order_release);
+    }
     for (auto& t : workers) t.join();
   }
   queue_weights();
