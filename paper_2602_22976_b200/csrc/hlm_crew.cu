@@ -46,6 +46,8 @@ constexpr uint32_t kNoEdge = 0xFFFFFFFFu;
 constexpr uint32_t kLightDeg = 32;
 constexpr uint32_t kMidDeg = 2048;
 
+struct C2Ctl;
+
 struct CrewState {
   unsigned long long* wkey = nullptr;  // m: weight bits of active edges, 0 otherwise
   uint8_t* estat = nullptr;            // m: EdgeStatus (matching.hpp:50)
@@ -75,6 +77,12 @@ struct CrewState {
   uint32_t* task_len = nullptr;     // live length
   unsigned long long* part_key = nullptr;  // per task: best key of the chunk
   uint32_t* part_id = nullptr;
+  C2Ctl* rc = nullptr;         // device-resident loop state
+  cudaGraph_t graph = nullptr;           // [round 1] -> WHILE { later rounds }
+  cudaGraphExec_t graph_exec = nullptr;
+  uint32_t graph_head_launches = 0, graph_body_launches = 0;
+  int graph_km = -1;
+  void* graph_params = nullptr;  // malloc'ed copy of the Crew2Params the graph was captured with
   // ---- edge-partitioned runs (hlm_shard.inc) ----
   unsigned long long* lkey = nullptr;  // n: this shard's maximum at every live vertex (live-slot order)
   uint32_t* mnow = nullptr;            // m bits: matched in the round in progress, not yet committed
@@ -297,6 +305,10 @@ void crew_release(Graph* g) {
   pool_free(c->task_len);
   pool_free(c->part_key);
   pool_free(c->part_id);
+  pool_free(c->rc);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  std::free(c->graph_params);
   pool_free(c->lkey);
   pool_free(c->mnow);
   delete c;
