@@ -15,8 +15,10 @@ FULL = [
     ("config 2: RMAT scale 24, 2^28 edges", dict(family="rmat", scale=24, m=1 << 28, seed=1, int_weights=True)),
     ("config 4: netlist n=10M, m=20M, sizes <= 4096", dict(family="netlist", n=10_000_000, m=20_000_000, seed=1, int_weights=True)),
     ("config 3: power-law n=50M, m=100M, sizes 2-64", dict(family="powerlaw", n=50_000_000, m=100_000_000, seed=1)),
-    # config 5 (16 G pins over 8 GPUs) has no CPU run; one GPU's shard shape at 1/10 of its size does
+    # config 5 (16 G pins over 8 GPUs) has no CPU run; what one of its 8 GPUs holds at weak scaling does
+    # (2 G pins: the reference's copy takes ~50 GB of host memory, skipped where that is not available)
     ("config 5 shard shape / 10: 8-uniform n=12.5M, m=25M", dict(family="uniform", n=12_500_000, m=25_000_000, d=8, seed=1)),
+    ("config 5 single-GPU shard shape: 8-uniform n=125M, m=250M", dict(family="uniform", n=125_000_000, m=250_000_000, d=8, seed=1)),
 ]
 
 
@@ -71,3 +73,37 @@ def test_full_size_matching_equals_the_reference(hb, ref, name, spec):
     assert want.per_round_deactivated == got.report.deactivated_per_round
     assert np.array_equal(want.matched_edges, got.matching.matched_edges)
     assert want.total_weight == got.matching.total_weight
+
+
+def test_edge_partitioned_run_at_the_shard_shape(hb):
+    """hlm_b200_match_sharded at full size: the 8-uniform shard shape as one shard through a one-rank NCCL
+    communicator and as two co-located shards must equal the single-instance matching; the true shard of
+    config 5 at 8 GPUs (250 M edges over n = 10^9 replicated vertices) must be a valid maximal matching."""
+    from paper_2602_22976_b200 import multi_gpu
+
+    spec = dict(n=125_000_000, m=250_000_000, d=8, seed=1)
+    s = hb.WeightStream()
+    whole = hb.DeviceHypergraph.generate("uniform", **spec)
+    want = whole.match(s, hb.ParallelConfig(variant="auto"))
+    whole.release()
+    comm = multi_gpu.Communicator.create(None, 0, 1, 0)
+    for world, c in ((1, comm), (2, None)):
+        shards = multi_gpu.generate_shards("uniform", world, **spec)
+        got, rep = multi_gpu.match_sharded(shards, s, hb.ParallelConfig(), c)
+        for g in shards:
+            g.release()
+        assert np.array_equal(got.matching.matched_edges, want.matching.matched_edges), world
+        assert got.report.matched_per_round_count == want.report.matched_per_round_count
+        assert got.report.deactivated_per_round == want.report.deactivated_per_round
+        assert got.matching.total_weight == want.matching.total_weight
+        assert rep["tie_redo_rounds"] == 0 and rep["host_syncs"] == rep["rounds"]
+        moved = rep["collective_bytes_per_round"]
+        assert moved == sorted(moved, reverse=True) and moved[-1] < moved[0] / 50
+    comm.destroy()
+    # rank 0's shard of config 5 at 8 GPUs: n = 10^9 vertices, edges [0, 250 M) of the 2 G
+    shard = hb.DeviceHypergraph.generate("uniform", n=1_000_000_000, m=2_000_000_000, d=8, seed=1, edge_begin=0, m_local=250_000_000)
+    got, rep = multi_gpu.match_sharded([shard], s, hb.ParallelConfig())
+    v = shard.verify(got.matching.matched_edges)
+    shard.release()
+    assert v.disjoint and v.maximal and v.weight == got.matching.total_weight
+    assert sum(got.report.matched_per_round_count) + sum(got.report.deactivated_per_round) == 250_000_000
