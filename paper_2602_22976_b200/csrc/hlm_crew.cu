@@ -47,6 +47,38 @@ constexpr uint32_t kLightDeg = 32;
 constexpr uint32_t kMidDeg = 2048;
 
 struct C2Ctl;
+struct ShCtl;
+
+// exchange arrays of an edge-partitioned run on one device (hlm_shard.inc); kept with the first shard
+// of the device between matchings
+struct ShDevMem {
+  uint32_t n = 0;
+  unsigned long long* gkey = nullptr;
+  unsigned long long* g2 = nullptr;
+  uint32_t* xv = nullptr;
+  uint32_t* lbits = nullptr;
+  uint32_t* lrank = nullptr;
+  uint32_t* hmax = nullptr;
+  uint32_t* bsum = nullptr;
+  uint32_t* counters = nullptr;
+  unsigned long long* c64 = nullptr;
+  ShCtl* ctl = nullptr;
+  ShCtl* h_ctl = nullptr;  // page-locked
+  void release() {
+    pool_free(gkey);
+    pool_free(g2);
+    pool_free(xv);
+    pool_free(lbits);
+    pool_free(lrank);
+    pool_free(hmax);
+    pool_free(bsum);
+    pool_free(counters);
+    pool_free(c64);
+    pool_free(ctl);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    *this = ShDevMem();
+  }
+};
 
 struct CrewState {
   unsigned long long* wkey = nullptr;  // m: weight bits of active edges, 0 otherwise
@@ -86,6 +118,7 @@ struct CrewState {
   // ---- edge-partitioned runs (hlm_shard.inc) ----
   unsigned long long* lkey = nullptr;  // n: this shard's maximum at every live vertex (live-slot order)
   uint32_t* mnow = nullptr;            // m bits: matched in the round in progress, not yet committed
+  ShDevMem shdev;                      // the device's exchange arrays, when this is its first shard
 };
 
 struct CrewParams {
@@ -311,6 +344,7 @@ void crew_release(Graph* g) {
   std::free(c->graph_params);
   pool_free(c->lkey);
   pool_free(c->mnow);
+  c->shdev.release();
   delete c;
   g->crew = nullptr;
 }

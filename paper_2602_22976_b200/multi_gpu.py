@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _lib
 from .api import (DeviceHypergraph, MatchResult, Matching, ParallelConfig, RoundLimitError, RunReport,
-                  WeightStream, WorkCounters, _raise, _take)
+                  WeightStream, WorkCounters, _borrow, _raise, _take)
 
 def shard_bounds(num_edges: int, world: int, rank: int):
     """Block partition of the edge ids: rank r owns [begin, begin + count)."""
@@ -105,6 +105,22 @@ class Communicator:
             pass
 
 
+class _ShardResults:
+    """Keeps the hlm_b200_result array of a sharded call alive while numpy views of it exist."""
+
+    def __init__(self, results, rep):
+        self.results, self.rep = results, rep
+
+    def __del__(self):
+        try:
+            lib = _lib.load_library()
+            for r in self.results:
+                lib.hlm_b200_result_free(C.byref(r))
+            lib.hlm_b200_shard_report_free(C.byref(self.rep))
+        except Exception:
+            pass
+
+
 def match_sharded(shards: List[DeviceHypergraph], stream: WeightStream, cfg: Optional[ParallelConfig] = None,
                   comm: Optional[Communicator] = None):
     """hlm_b200_match_sharded: the round loop, the collectives and the tie handling run inside the library.
@@ -119,30 +135,29 @@ def match_sharded(shards: List[DeviceHypergraph], stream: WeightStream, cfg: Opt
     cs, cc = stream._c(), cfg._c()
     st = lib.hlm_b200_match_sharded(handles, k, comm._h if comm else None, C.byref(cs), C.byref(cc), results,
                                     C.byref(rep))
-    try:
-        if st not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
-            _raise(st, "hlm_b200_match_sharded")
-        rounds = int(rep.rounds)
-        matched = np.concatenate([_take(r.matched_edges, r.num_matched, np.uint32) for r in results])
-        round_of = np.concatenate([_take(r.matched_round, r.num_matched, np.uint16) for r in results])
-        prm = _take(results[0].per_round_matched, rounds, np.uint32).tolist()
-        prd = _take(results[0].per_round_deactivated, rounds, np.uint32).tolist()
-        report = dict(rounds=rounds, num_local_shards=int(rep.num_local_shards), num_processes=int(rep.num_processes),
-                      tie_redo_rounds=int(rep.tie_redo_rounds), host_syncs=int(rep.host_syncs),
-                      kernel_launches=int(rep.kernel_launches), nccl_calls=int(rep.nccl_calls),
-                      num_edges_global=int(rep.num_edges_global), collective_bytes=int(rep.collective_bytes),
-                      collective_bytes_per_round=_take(rep.collective_bytes_per_round, rounds, np.uint64).tolist(),
-                      live_vertices_per_round=_take(rep.live_vertices_per_round, rounds, np.uint32).tolist())
-        matching = Matching(matched, float(results[0].total_weight), rounds, prm)
-        rr = RunReport(rounds, prm, prd, round_of,
-                       WorkCounters(rounds, sum(int(r.total_edge_visits) for r in results),
-                                    sum(int(r.total_pin_visits) for r in results)),
-                       float(results[0].wall_time_ms), 0, max(float(r.device_ms) for r in results), 0,
-                       int(rep.tie_redo_rounds), int(rep.kernel_launches), 0, matched)
-    finally:
-        for r in results:
-            lib.hlm_b200_result_free(C.byref(r))
-        lib.hlm_b200_shard_report_free(C.byref(rep))
+    owner = _ShardResults(results, rep)  # frees the C results when the last view of them is gone
+    if st not in (_lib.OK, _lib.ERR_ROUND_LIMIT):
+        _raise(st, "hlm_b200_match_sharded")
+    rounds = int(rep.rounds)
+    # views of the library's page-locked result arrays: no copy for one shard, one concatenation otherwise
+    ids = [_borrow(owner, r.matched_edges, r.num_matched, C.c_uint32, np.uint32) for r in results]
+    rnd = [_borrow(owner, r.matched_round, r.num_matched, C.c_uint16, np.uint16) for r in results]
+    matched = ids[0] if k == 1 else np.concatenate(ids)
+    round_of = rnd[0] if k == 1 else np.concatenate(rnd)
+    prm = _take(results[0].per_round_matched, rounds, np.uint32).tolist()
+    prd = _take(results[0].per_round_deactivated, rounds, np.uint32).tolist()
+    report = dict(rounds=rounds, num_local_shards=int(rep.num_local_shards), num_processes=int(rep.num_processes),
+                  tie_redo_rounds=int(rep.tie_redo_rounds), host_syncs=int(rep.host_syncs),
+                  kernel_launches=int(rep.kernel_launches), nccl_calls=int(rep.nccl_calls),
+                  num_edges_global=int(rep.num_edges_global), collective_bytes=int(rep.collective_bytes),
+                  collective_bytes_per_round=_take(rep.collective_bytes_per_round, rounds, np.uint64).tolist(),
+                  live_vertices_per_round=_take(rep.live_vertices_per_round, rounds, np.uint32).tolist())
+    matching = Matching(matched, float(results[0].total_weight), rounds, prm)
+    rr = RunReport(rounds, prm, prd, round_of,
+                   WorkCounters(rounds, sum(int(r.total_edge_visits) for r in results),
+                                sum(int(r.total_pin_visits) for r in results)),
+                   float(results[0].wall_time_ms), 0, max(float(r.device_ms) for r in results), 0,
+                   int(rep.tie_redo_rounds), int(rep.kernel_launches), 0, matched)
     if st == _lib.ERR_ROUND_LIMIT:
         raise RoundLimitError(matching, rr)
     return MatchResult(matching, rr), report
