@@ -91,7 +91,8 @@ struct Graph {
   // vertex -> incident edges, built on the device when a variant (crew) or a download needs it
   uint64_t* voff = nullptr;  // n+1
   uint32_t* vinc = nullptr;  // kappa
-  bool vinc_flagged = false;  // bit 31 of an entry: the list's vertex is the first pin of that edge (m < 2^31)
+  bool vinc_flagged = false;  // bit 31 of an entry: the list's vertex is the proposer of that edge (m < 2^31)
+  bool vinc_first_pin = true;  // the proposer is the edge's first pin (else: its pin with the smallest vertex id)
   uint64_t device_bytes = 0;
   uint64_t h2d_bytes = 0;
   int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0;

@@ -177,26 +177,41 @@ __global__ void k_copy_u64(const unsigned long long* in, uint64_t count, unsigne
 }
 
 // pos[v] starts as voff[v]; the returning 64-bit add hands out the slots of v's list
-// flag_first: bit 31 of the entry written for an edge's FIRST pin is set (the vertex-owned matching
-// kernels use it to decide for free whether a vertex is the first pin of its argmax)
+// flag_mode != 0: bit 31 of the entry written for ONE pin of every edge is set -- its proposer: the
+// vertex-owned matching kernels look at an edge only when the proposer names it as its argmax.
+// 1: the first pin; 2: the pin with the smallest vertex id, which on an instance renumbered by
+// descending degree is the pin with the most incident edges, i.e. the one least likely to name a
+// given edge (fewest proposals to check).
 __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, uint32_t vhi, unsigned long long* pos,
-                                 const uint32_t* orig, uint32_t* vinc, bool flag_first) {
+                                 const uint32_t* orig, uint32_t* vinc, int flag_mode) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     uint64_t b;
     uint32_t s;
     csr.range(e, b, s);
     uint32_t id = 0xffffffffu;  // incidence lists name edges by the caller's ids
+    uint32_t proposer = 0;
+    if (flag_mode == 2) {
+      uint32_t best = 0xffffffffu;
+      for (uint32_t i = 0; i < s; ++i) {
+        const uint32_t v = __ldcs(csr.pins + b + i);
+        if (v < best) {
+          best = v;
+          proposer = i;
+        }
+      }
+      if (best < vlo || best >= vhi) proposer = 0xffffffffu;  // flagged by the pass that owns that vertex
+    }
     for (uint32_t i = 0; i < s; ++i) {
       const uint32_t v = __ldcs(csr.pins + b + i);
       if (v < vlo || v >= vhi) continue;
       if (id == 0xffffffffu) id = orig ? orig[e] : e;
-      vinc[atomicAdd(pos + v, 1ull)] = (flag_first && i == 0) ? (id | 0x80000000u) : id;
+      vinc[atomicAdd(pos + v, 1ull)] = (flag_mode != 0 && i == proposer) ? (id | 0x80000000u) : id;
     }
   }
 }
 
 // voff (n+1) / vinc (kappa) of the CSR `csr` over n vertices; edges are named by orig[] when given
-static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc, bool flag_first = false) {
+static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc, int flag_mode = 0) {
   cudaStream_t s = g->stream;
   const bool trace = std::getenv("HLM_B200_TRACE") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
@@ -233,7 +248,7 @@ static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, ui
     for (uint64_t lo = 0; lo < g->n; lo += win8)
       k_fill_incidence<<<grid_of(g, g->m), kBlock, 0, s>>>(csr, g->m, static_cast<uint32_t>(lo),
                                                            static_cast<uint32_t>(std::min<uint64_t>(g->n, lo + win8)), pos,
-                                                           g->orig, vinc, flag_first);
+                                                           g->orig, vinc, flag_mode);
     CU_CHECK(cudaStreamSynchronize(s));
     mark("fill");
     pool_free(pos);
@@ -251,7 +266,10 @@ int build_incidence(Graph* g) {
   g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
   CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 16, g->stream));
   g->vinc_flagged = g->m < 0x7fffffffu;
-  return build_incidence_into(g, g->csr(), g->voff, g->vinc, g->vinc_flagged);
+  // proposer of an edge: its highest-degree pin where vertex ids are degree ranks (renumbered, ragged
+  // instances: an order of magnitude fewer proposals on skewed degrees), else its first pin
+  g->vinc_first_pin = !(g->vold && !g->uniform_d) || std::getenv("HLM_B200_PROPOSER_FIRST") != nullptr;
+  return build_incidence_into(g, g->csr(), g->voff, g->vinc, !g->vinc_flagged ? 0 : g->vinc_first_pin ? 1 : 2);
 }
 
 // ---------------------------------------------------------------------------------------------
