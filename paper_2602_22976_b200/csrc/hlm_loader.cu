@@ -262,9 +262,9 @@ static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, ui
 int build_incidence(Graph* g) {
   if (g->voff) return HLM_B200_OK;
   ST_CHECK(dalloc(&g->voff, static_cast<size_t>(g->n) + 1));
-  ST_CHECK(dalloc(&g->vinc, g->kappa + 4));  // one quad of padding: the CREW sweep loads 16 bytes at a time
+  ST_CHECK(dalloc(&g->vinc, g->kappa + 16));  // padding: the vertex-owned sweep copies windows that end on a multiple of 16 entries
   g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
-  CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 16, g->stream));
+  CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 64, g->stream));
   g->vinc_flagged = g->m < 0x7fffffffu;
   // proposer of an edge: its highest-degree pin where vertex ids are degree ranks (renumbered, ragged
   // instances: an order of magnitude fewer proposals on skewed degrees), else its first pin
