@@ -424,20 +424,6 @@ int new_graph(int device, Graph** out) {
 // uniformity and pack the weights to one byte each; what passes is not uploaded (offsets) or
 // uploaded packed and widened on the device (weights).  Anything else takes the plain path.
 // ---------------------------------------------------------------------------------------------
-// HLM_B200_TRACE=1: phase times of the loader / one-shot call on stderr
-struct PhaseTrace {
-  bool on = std::getenv("HLM_B200_TRACE") != nullptr;
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[hlm_b200] %-28s %8.2f ms  (+%.2f)\n", what,
-                 std::chrono::duration<double, std::milli>(now - t0).count(),
-                 std::chrono::duration<double, std::milli>(now - last).count());
-    last = now;
-  }
-};
-
 struct UploadPlan {
   bool reorder = true;      // sort the resident edges by first pin (pays off after ~30 matchings)
   bool host_assist = true;  // use the host cores as described above

@@ -1,6 +1,9 @@
 // hlm_engine.h -- host-side types shared by the translation units of libhlm_b200.so.
 #pragma once
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/hlm_b200.h"
@@ -61,6 +64,21 @@ struct Workspace {
 };
 
 struct CrewState;  // hlm_crew.cu
+
+// HLM_B200_TRACE=1: phase times of the loader / a matching on stderr (host clock; `sync` waits for the stream first)
+struct PhaseTrace {
+  bool on = std::getenv("HLM_B200_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what, cudaStream_t sync = nullptr) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(sync);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hlm_b200] %-28s %8.2f ms  (+%.2f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - t0).count(),
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
 
 // An instance resident in HBM (pin-CSR as 32-bit arrays, optional incidence-CSR).
 struct Graph {

@@ -210,6 +210,148 @@ __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, ui
   }
 }
 
+// ---- two-level slot fill ----
+// The windowed fill above keeps the cursors in L2 but still scatters its 4-byte writes over a list region
+// of hundreds of MB per pass (8-uniform shard shape: 235 ms for 2 G entries).  Here the (vertex, entry)
+// pairs are first PARTITIONED by vertex range into buckets whose list region fits L2 (a radix pass: per-CTA
+// histogram in shared memory, one range reservation per CTA and bucket, runs of pairs written back to
+// back), then every bucket is filled on its own: its cursors and its slice of the list array stay in L2
+// and reach HBM once.
+constexpr uint32_t kIncMaxBuckets = 4096;
+constexpr uint32_t kIncEdgesPerThread = 8;
+
+__global__ void k_inc_bucket_cursors(const unsigned long long* voff, uint32_t n, uint32_t shift, uint32_t buckets,
+                                     unsigned long long* bcur) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < buckets; b += gridDim.x * blockDim.x) {
+    const unsigned long long first = static_cast<unsigned long long>(b) << shift;
+    bcur[b] = voff[first < n ? first : n];
+  }
+}
+
+__device__ __forceinline__ uint32_t inc_proposer(const EdgeCsr& csr, uint64_t b, uint32_t s, int flag_mode) {
+  if (flag_mode != 2) return 0u;
+  uint32_t best = 0xffffffffu, at = 0u;
+  for (uint32_t i = 0; i < s; ++i) {
+    const uint32_t v = __ldg(csr.pins + b + i);
+    if (v < best) {
+      best = v;
+      at = i;
+    }
+  }
+  return at;
+}
+
+__global__ void __launch_bounds__(kBlock) k_inc_partition(const EdgeCsr csr, uint32_t m, const uint32_t* orig, uint32_t shift,
+                                                          uint32_t buckets, unsigned long long* bcur, int flag_mode,
+                                                          unsigned long long* pairs) {
+  extern __shared__ unsigned long long s_mem[];
+  unsigned long long* s_base = s_mem;                                  // [buckets]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mem + buckets);      // [buckets]
+  const uint32_t per_block = kBlock * kIncEdgesPerThread;
+  for (uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * per_block; e0 < m; e0 += static_cast<uint64_t>(gridDim.x) * per_block) {
+    for (uint32_t b = threadIdx.x; b < buckets; b += kBlock) s_cnt[b] = 0u;
+    __syncthreads();
+    for (uint32_t k = 0; k < kIncEdgesPerThread; ++k) {
+      const uint64_t e = e0 + threadIdx.x + static_cast<uint64_t>(k) * kBlock;
+      if (e >= m) break;
+      uint64_t b;
+      uint32_t s;
+      csr.range(static_cast<uint32_t>(e), b, s);
+      for (uint32_t i = 0; i < s; ++i) atomicAdd(s_cnt + (__ldg(csr.pins + b + i) >> shift), 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < buckets; b += kBlock) {
+      const uint32_t c = s_cnt[b];
+      s_base[b] = c ? atomicAdd(bcur + b, static_cast<unsigned long long>(c)) : 0ull;
+      s_cnt[b] = 0u;
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < kIncEdgesPerThread; ++k) {
+      const uint64_t e = e0 + threadIdx.x + static_cast<uint64_t>(k) * kBlock;
+      if (e >= m) break;
+      uint64_t b;
+      uint32_t s;
+      csr.range(static_cast<uint32_t>(e), b, s);
+      const uint32_t id = orig ? orig[e] : static_cast<uint32_t>(e);
+      const uint32_t proposer = inc_proposer(csr, b, s, flag_mode);
+      for (uint32_t i = 0; i < s; ++i) {
+        const uint32_t v = __ldg(csr.pins + b + i);
+        const uint32_t bk = v >> shift;
+        const uint32_t raw = (flag_mode != 0 && i == proposer) ? (id | 0x80000000u) : id;
+        pairs[s_base[bk] + atomicAdd(s_cnt + bk, 1u)] = (static_cast<unsigned long long>(v) << 32) | raw;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// pairs [begin, end): the entries of the vertices of a few consecutive buckets
+__global__ void __launch_bounds__(kBlock) k_inc_fill_bucket(const unsigned long long* pairs, unsigned long long begin,
+                                                            unsigned long long end, unsigned long long* pos, uint32_t* vinc) {
+  for (unsigned long long p = begin + blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; p < end;
+       p += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long pr = __ldcs(pairs + p);
+    vinc[atomicAdd(pos + (pr >> 32), 1ull)] = static_cast<uint32_t>(pr);
+  }
+}
+
+// true if the two-level fill ran (false: not enough memory for the pair array, or nothing to gain)
+static int fill_incidence_partitioned(Graph* g, const EdgeCsr& csr, const uint64_t* voff, uint32_t* vinc, int flag_mode,
+                                      bool* done) {
+  *done = false;
+  if (g->kappa < (1ull << 26) || std::getenv("HLM_B200_INCIDENCE_WINDOWED")) return HLM_B200_OK;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return HLM_B200_OK;
+  const size_t need = g->kappa * 8 + static_cast<size_t>(g->n) * 8 + (64u << 20);
+  if (need > free_b) return HLM_B200_OK;
+  cudaStream_t s = g->stream;
+  // buckets: list region of about a quarter of L2, at most kIncMaxBuckets of them (shared-memory histogram)
+  const double avg = static_cast<double>(g->kappa) / std::max<uint32_t>(1, g->n);
+  uint32_t shift = 10;
+  while (shift < 31 && (static_cast<double>(1ull << shift) * avg * 4.0 < static_cast<double>(g->l2_bytes) / 4.0)) ++shift;
+  while (((static_cast<uint64_t>(g->n) + (1ull << shift) - 1) >> shift) > kIncMaxBuckets) ++shift;
+  const uint32_t buckets = static_cast<uint32_t>((static_cast<uint64_t>(g->n) + (1ull << shift) - 1) >> shift);
+  unsigned long long *pairs = nullptr, *bcur = nullptr, *pos = nullptr;
+  int rc = dalloc(&pairs, g->kappa);
+  if (rc == HLM_B200_OK) rc = dalloc(&bcur, buckets);
+  if (rc == HLM_B200_OK) rc = dalloc(&pos, g->n);
+  if (rc != HLM_B200_OK) {
+    pool_free(pairs);
+    pool_free(bcur);
+    pool_free(pos);
+    cudaGetLastError();
+    return HLM_B200_OK;  // fall back to the windowed fill
+  }
+  const unsigned long long* voffu = reinterpret_cast<const unsigned long long*>(voff);
+  k_inc_bucket_cursors<<<grid_of(g, buckets), kBlock, 0, s>>>(voffu, g->n, shift, buckets, bcur);
+  const size_t smem = static_cast<size_t>(buckets) * 12;
+  cudaFuncSetAttribute(k_inc_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_inc_partition<<<g->num_sms * 4, kBlock, smem, s>>>(csr, g->m, g->orig, shift, buckets, bcur, flag_mode, pairs);
+  k_copy_u64<<<grid_of(g, g->n), kBlock, 0, s>>>(voffu, g->n, pos);
+  // bucket boundaries on the host: voff at every bucket start (bcur is done with: reuse it, + the end)
+  std::vector<unsigned long long> bounds(static_cast<size_t>(buckets) + 1);
+  k_inc_bucket_cursors<<<grid_of(g, buckets), kBlock, 0, s>>>(voffu, g->n, shift, buckets, bcur);
+  CU_CHECK(cudaMemcpyAsync(bounds.data(), bcur, static_cast<size_t>(buckets) * 8, cudaMemcpyDeviceToHost, s));
+  CU_CHECK(cudaMemcpyAsync(&bounds[buckets], voffu + g->n, 8, cudaMemcpyDeviceToHost, s));
+  CU_CHECK(cudaStreamSynchronize(s));
+  // fill: a few buckets per launch so that their list slices and cursors stay in L2 together
+  const unsigned long long per_launch = static_cast<unsigned long long>(g->l2_bytes) / 2 / 4;  // entries
+  for (uint32_t b = 0; b < buckets;) {
+    uint32_t e = b + 1;
+    while (e < buckets && bounds[e + 1] - bounds[b] <= per_launch) ++e;
+    const unsigned long long cnt = bounds[e] - bounds[b];
+    if (cnt) k_inc_fill_bucket<<<grid_of(g, cnt), kBlock, 0, s>>>(pairs, bounds[b], bounds[e], pos, vinc);
+    b = e;
+  }
+  CU_CHECK(cudaStreamSynchronize(s));
+  pool_free(pairs);
+  pool_free(bcur);
+  pool_free(pos);
+  CU_CHECK(cudaGetLastError());
+  *done = true;
+  return HLM_B200_OK;
+}
+
 // voff (n+1) / vinc (kappa) of the CSR `csr` over n vertices; edges are named by orig[] when given
 static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, uint32_t* vinc, int flag_mode = 0) {
   cudaStream_t s = g->stream;
@@ -241,7 +383,10 @@ static int build_incidence_into(Graph* g, const EdgeCsr& csr, uint64_t* voff, ui
   pool_free(deg);
   if (rc != HLM_B200_OK) return rc;
   mark("scan");
-  if (g->m && g->n) {
+  bool partitioned = false;
+  if (g->m && g->n) ST_CHECK(fill_incidence_partitioned(g, csr, voff, vinc, flag_mode, &partitioned));
+  if (partitioned) mark("fill (two-level)");
+  if (g->m && g->n && !partitioned) {
     unsigned long long* pos = nullptr;
     ST_CHECK(dalloc(&pos, g->n));
     k_copy_u64<<<grid_of(g, g->n), kBlock, 0, s>>>(reinterpret_cast<const unsigned long long*>(voff), g->n, pos);
