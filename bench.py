@@ -349,7 +349,7 @@ def measure(hb, torch, np, dg, wl, steps, warmup, tstream, hbm_gbs):
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
     ms_per_step = total_ms / steps
-    crcw_engine = res.report.graph_launches > 0
+    crcw_engine = res.report.engine == "crcw"
     # per-kernel times: host-driven loop, CUDA events around every launch, best of 3
     prof_cfg = hb.ParallelConfig(variant="auto", loop_mode="host", kernel_times=True)
     sweep_ms = rest_ms = None
@@ -370,9 +370,13 @@ def measure(hb, torch, np, dg, wl, steps, warmup, tstream, hbm_gbs):
                   "round sweep of the CRCW engine: k_filter_vmax_small / k_filter_vmax_large") + \
             ": invalidate + compact + key + vertex-max atomics"
     else:
-        sweep_bytes = vs
+        # vertex-owned rounds: the vertex-max sweep over the incidence lists; after the hand-over (if any) the
+        # CRCW round sweep, each with its own share of the algorithmic bytes
+        sw = res.report.engine_switch_round or (len(vs) + 1)
+        sweep_bytes = [vs[q] if q + 1 < sw else fb[q] for q in range(len(vs))]
         kernel = ("vertex-max sweep of the vertex-owned engine: k_c2_argmax_light<MODE,KM> (+ k_c2_argmax_task / "
-                  "k_c2_argmax_heavy for lists > 256 entries): list walk + alive filter + key + argmax + compaction")
+                  "k_c2_argmax_heavy for lists > 256 entries): list walk + alive filter + key + argmax + compaction"
+                  + (f"; from round {sw} the CRCW round sweep (few edges left)" if res.report.engine_switch_round else ""))
     nl = len(sweep_bytes)
     sweep_total_ms = float(sweep_ms[:nl].sum())
     rest_total_ms = float(rest_ms[:nl].sum())
@@ -388,7 +392,7 @@ def measure(hb, torch, np, dg, wl, steps, warmup, tstream, hbm_gbs):
                               "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_gbs}}
     out = dict(kappa=kappa, m=m, n=n, ms_per_step=ms_per_step, total_ms=total_ms, value=kappa * steps / (total_ms * 1e-3),
                launches=int(launches), dev_ms=float(np.mean(dev_ms)), res=res, roofline=roofline,
-               engine="crcw (CUDA-graph WHILE loop)" if crcw_engine else "vertex-owned / crew kernels (host-driven loop)")
+               engine=res.report.engine + " (one CUDA-graph launch per matching)")
     return out
 
 

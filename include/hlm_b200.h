@@ -132,7 +132,12 @@ typedef struct {
   uint64_t h2d_bytes;              /* hlm_b200_match_host: bytes the loader moved host -> device */
   uint32_t prefix_sum_invocations; /* WorkCounters (matching.hpp:27-33): non-zero for WORK_OPTIMAL only */
   uint32_t compactions;
+  uint32_t engine;                 /* HLM_B200_ENGINE_*: which kernels ran (what HLM_B200_VARIANT_AUTO chose) */
+  uint32_t engine_switch_round;    /* HLM_B200_ENGINE_VERTEX_THEN_CRCW: first round on the CRCW kernels, else 0 */
 } hlm_b200_result;
+
+enum { HLM_B200_ENGINE_CRCW = 1, HLM_B200_ENGINE_VERTEX_OWNED = 2, HLM_B200_ENGINE_VERTEX_THEN_CRCW = 3,
+       HLM_B200_ENGINE_SHARDED = 4 };
 
 typedef struct hlm_b200_graph hlm_b200_graph; /* opaque: instance resident in HBM */
 

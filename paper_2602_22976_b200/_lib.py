@@ -39,7 +39,8 @@ class Result(C.Structure):
                 ("tie_redo_rounds", C.c_uint32), ("kernel_launches", C.c_uint32),
                 ("graph_launches", C.c_uint32), ("write_conflicts", C.c_uint32),
                 ("round_filter_ms", C.POINTER(C.c_float)), ("round_check_ms", C.POINTER(C.c_float)),
-                ("h2d_bytes", C.c_uint64), ("prefix_sum_invocations", C.c_uint32), ("compactions", C.c_uint32)]
+                ("h2d_bytes", C.c_uint64), ("prefix_sum_invocations", C.c_uint32), ("compactions", C.c_uint32),
+                ("engine", C.c_uint32), ("engine_switch_round", C.c_uint32)]
 
 
 class GraphInfo(C.Structure):

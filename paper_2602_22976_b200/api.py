@@ -136,6 +136,8 @@ class RunReport:
     round_filter_ms: Optional[List[float]] = None
     round_check_ms: Optional[List[float]] = None
     h2d_bytes: int = 0  # run_variant (host arrays in): bytes the loader moved host -> device
+    engine: str = ""    # which kernels ran: "crcw" | "vertex-owned" | "vertex-owned, crcw from round k" | "sharded"
+    engine_switch_round: int = 0
 
     @property
     def matched_per_round(self) -> List[np.ndarray]:
@@ -217,7 +219,9 @@ def _convert(status: int, res: _lib.Result) -> MatchResult:
                        int(res.graph_launches), matched,
                        _take(res.round_filter_ms, res.rounds + 1, np.float32).tolist() if res.round_filter_ms else None,
                        _take(res.round_check_ms, res.rounds + 1, np.float32).tolist() if res.round_check_ms else None,
-                       int(res.h2d_bytes))
+                       int(res.h2d_bytes),
+                       {1: "crcw", 2: "vertex-owned", 3: f"vertex-owned, crcw from round {int(res.engine_switch_round)}",
+                        4: "sharded"}.get(int(res.engine), ""), int(res.engine_switch_round))
     if status == _lib.ERR_ROUND_LIMIT:
         raise RoundLimitError(matching, report)
     return MatchResult(matching, report)

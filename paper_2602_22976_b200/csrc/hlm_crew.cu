@@ -452,6 +452,7 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
     CU_CHECK(cudaMemcpyAsync(w.deact_cnt + 1, dropped_r.data(), round * 4ull, cudaMemcpyHostToDevice, s));
   }
   out->kernel_launches = launches;
+  out->engine = HLM_B200_ENGINE_VERTEX_OWNED;
   out->device_edge_visits = static_cast<uint64_t>(g->m) * round;
   int rc = assemble_result(g, round, cfg, report_variant, out);
   if (rc != HLM_B200_OK) return rc;

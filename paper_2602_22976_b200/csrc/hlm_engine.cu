@@ -1236,6 +1236,100 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   return HLM_B200_OK;
 }
 
+struct CrcwRunStats {
+  uint32_t tie_redo = 0, graph_launches = 0, graph_kernels = 0;
+  std::vector<float> t_filter, t_check;  // per round, host loop with want_times
+};
+
+// The CRCW round loop from the state in `c` / w.ctrl (already on the device) to termination, the round cap,
+// or an error: one CUDA-graph launch per stretch of rounds (from_round1: the graph that starts with the
+// specialised round-1 sweep; otherwise the WHILE node alone, which resumes at any round), or the host-driven
+// loop; tied rounds are redone on the exact path, tag wraps are cleared.  `c` ends as the final Ctrl.
+static int crcw_run(Graph* g, Launcher& L, uint32_t max_rounds, bool use_graph, bool from_round1, bool want_times,
+                    Ctrl& c, CrcwRunStats& S) {
+  Workspace& w = g->ws;
+  cudaStream_t s = g->stream;
+  bool in_graph = false;
+  Ctrl c_before = c;
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  if (want_times)
+    for (auto& ev : tev) CU_CHECK(cudaEventCreate(&ev));
+  uint32_t& tie_redo = S.tie_redo;
+  uint32_t& graph_launches = S.graph_launches;
+  uint32_t& graph_kernels = S.graph_kernels;
+  std::vector<float>& t_filter = S.t_filter;
+  std::vector<float>& t_check = S.t_check;
+  {
+    for (;;) {
+      if (use_graph) {
+        // one launch runs every round; it only comes back early for a tie or a tag wrap, and the
+        // run is then resumed with the WHILE node alone (the full graph starts at round 1)
+        const int which = (from_round1 && graph_launches == 0) ? 0 : 1;
+        if (!w.graph_exec[which]) ST_CHECK(build_loop_graph(L, which));
+        c_before = c;
+        CU_CHECK(cudaGraphLaunch(w.graph_exec[which], s));
+        ++graph_launches;
+        in_graph = true;
+      } else if (L.exact) {
+        L.filter<false>(s);
+        // the exact levels need the list lengths on the host
+        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_CHECK(cudaStreamSynchronize(s));
+        if (c.round <= max_rounds) ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
+        L.advance(s, 0, 0);
+      } else {
+        if (want_times) CU_CHECK(cudaEventRecord(tev[0], s));
+        L.filter<true>(s, c.round == 1);
+        if (want_times) CU_CHECK(cudaEventRecord(tev[1], s));
+        L.check(s);
+        if (want_times) CU_CHECK(cudaEventRecord(tev[2], s));
+        L.advance(s, 0, 0);
+      }
+      CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+      CU_CHECK(cudaStreamSynchronize(s));
+      if (in_graph) {
+        in_graph = false;
+        // sweeps executed by this launch: rounds c_before.round .. last, where the last sweep is
+        // the one that found the lists empty / hit the cap / saw the tie (round not advanced)
+        const uint32_t last = c.status == ST_EPOCH ? c.round - 1u : c.round;
+        const uint32_t sweeps = last - c_before.round + 1u;
+        graph_kernels += (from_round1 && graph_launches == 1) ? w.graph_head_launches + (sweeps - 1u) * w.graph_body_launches
+                                                              : sweeps * w.graph_body_launches;
+      }
+      if (want_times) {
+        float a = 0.f, b = 0.f;
+        CU_CHECK(cudaEventElapsedTime(&a, tev[0], tev[1]));
+        CU_CHECK(cudaEventElapsedTime(&b, tev[1], tev[2]));
+        t_filter.push_back(a);
+        t_check.push_back(b);
+      }
+      if (c.status == ST_RUNNING) continue;
+      if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
+      if (c.status == ST_TIE) {
+        // a vertex saw two equal 64-bit keys in round c.round: redo that round exactly
+        ++tie_redo;
+        ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
+        CU_CHECK(cudaMemsetAsync(&w.ctrl->tie_flag, 0, 4, s));
+        L.advance(s, 0, 0);
+        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_CHECK(cudaStreamSynchronize(s));
+        if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
+        if (c.status == ST_TIE) {
+          set_error("internal: tie flag survived the exact redo");
+          return HLM_B200_ERR_CUDA;
+        }
+      }
+      if (c.status == ST_EPOCH) {
+        k_epoch_reset<<<grid_for(g, g->n), kBlock, 0, s>>>(w.vkey, w.vtop, g->n);
+        ++L.launches;
+      }
+    }
+  }
+  for (auto& ev : tev)
+    if (ev) cudaEventDestroy(ev);
+  return HLM_B200_OK;
+}
+
 int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {
   // greedy_sorted (local_max_seq.hpp:130-152) is the lexicographically first maximal matching under
   // the static order (weight descending, id ascending).  Repeating "every edge that is first in
@@ -1290,93 +1384,25 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
 
   Ctrl c = c0;
-  uint32_t tie_redo = 0, graph_launches = 0, graph_kernels = 0;
-  bool in_graph = false;
-  Ctrl c_before = c0;
+  CrcwRunStats S;
   const bool want_times = (cfg->flags & HLM_B200_FLAG_KERNEL_TIMES) && !use_graph && !L.exact;
-  std::vector<float> t_filter, t_check;
-  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
-  if (want_times)
-    for (auto& ev : tev) CU_CHECK(cudaEventCreate(&ev));
-  if (g->m == 0) {
+  if (g->m == 0)
     c.status = ST_DONE;
-  } else {
-    for (;;) {
-      if (use_graph) {
-        // one launch runs every round; it only comes back early for a tie or a tag wrap, and the
-        // run is then resumed with the WHILE node alone (the full graph starts at round 1)
-        const int which = graph_launches == 0 ? 0 : 1;
-        if (!w.graph_exec[which]) ST_CHECK(build_loop_graph(L, which));
-        c_before = c;
-        CU_CHECK(cudaGraphLaunch(w.graph_exec[which], s));
-        ++graph_launches;
-        in_graph = true;
-      } else if (L.exact) {
-        L.filter<false>(s);
-        // the exact levels need the list lengths on the host
-        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
-        CU_CHECK(cudaStreamSynchronize(s));
-        if (c.round <= max_rounds) ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
-        L.advance(s, 0, 0);
-      } else {
-        if (want_times) CU_CHECK(cudaEventRecord(tev[0], s));
-        L.filter<true>(s, c.round == 1);
-        if (want_times) CU_CHECK(cudaEventRecord(tev[1], s));
-        L.check(s);
-        if (want_times) CU_CHECK(cudaEventRecord(tev[2], s));
-        L.advance(s, 0, 0);
-      }
-      CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
-      CU_CHECK(cudaStreamSynchronize(s));
-      if (in_graph) {
-        in_graph = false;
-        // sweeps executed by this launch: rounds c_before.round .. last, where the last sweep is
-        // the one that found the lists empty / hit the cap / saw the tie (round not advanced)
-        const uint32_t last = c.status == ST_EPOCH ? c.round - 1u : c.round;
-        const uint32_t sweeps = last - c_before.round + 1u;
-        graph_kernels += graph_launches == 1 ? w.graph_head_launches + (sweeps - 1u) * w.graph_body_launches
-                                             : sweeps * w.graph_body_launches;
-      }
-      if (want_times) {
-        float a = 0.f, b = 0.f;
-        CU_CHECK(cudaEventElapsedTime(&a, tev[0], tev[1]));
-        CU_CHECK(cudaEventElapsedTime(&b, tev[1], tev[2]));
-        t_filter.push_back(a);
-        t_check.push_back(b);
-      }
-      if (c.status == ST_RUNNING) continue;
-      if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
-      if (c.status == ST_TIE) {
-        // a vertex saw two equal 64-bit keys in round c.round: redo that round exactly
-        ++tie_redo;
-        ST_CHECK(exact_round(L, c.round, c.parity ^ 1u, c));
-        CU_CHECK(cudaMemsetAsync(&w.ctrl->tie_flag, 0, 4, s));
-        L.advance(s, 0, 0);
-        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
-        CU_CHECK(cudaStreamSynchronize(s));
-        if (c.status == ST_DONE || c.status == ST_ROUND_LIMIT) break;
-        if (c.status == ST_TIE) {
-          set_error("internal: tie flag survived the exact redo");
-          return HLM_B200_ERR_CUDA;
-        }
-      }
-      if (c.status == ST_EPOCH) {
-        k_epoch_reset<<<grid_for(g, g->n), kBlock, 0, s>>>(w.vkey, w.vtop, g->n);
-        ++L.launches;
-      }
-    }
-  }
+  else
+    ST_CHECK(crcw_run(g, L, max_rounds, use_graph, /*from_round1=*/true, want_times, c, S));
+  const uint32_t tie_redo = S.tie_redo, graph_launches = S.graph_launches, graph_kernels = S.graph_kernels;
+  std::vector<float>& t_filter = S.t_filter;
+  std::vector<float>& t_check = S.t_check;
   CU_CHECK(cudaGetLastError());
   const uint32_t rounds = c.rounds_done;
   out->tie_redo_rounds = tie_redo;
   out->graph_launches = graph_launches;
+  out->engine = HLM_B200_ENGINE_CRCW;
   out->device_edge_visits = c.edges_swept;
   out->device_pin_visits = c.pins_swept;
   g->ws.pins_matched = c.pins_matched;
   // kernels actually executed: host-launched ones plus (rounds + 1) graph bodies
   out->kernel_launches = L.launches + graph_kernels;
-  for (auto& ev : tev)
-    if (ev) cudaEventDestroy(ev);
   if (want_times) {
     out->round_filter_ms = static_cast<float*>(std::calloc(rounds + 2, sizeof(float)));
     out->round_check_ms = static_cast<float*>(std::calloc(rounds + 2, sizeof(float)));
@@ -1401,6 +1427,50 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     return HLM_B200_ERR_UNSUPPORTED;
   }
   return c.status == ST_ROUND_LIMIT ? HLM_B200_ERR_ROUND_LIMIT : HLM_B200_OK;
+}
+
+__global__ void k_tail_vertices(const uint32_t* dead, uint32_t* vtop, unsigned long long* vkey, uint32_t n) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    vtop[v] = ((dead[v >> 5] >> (v & 31u)) & 1u) ? kTopDead : 0u;
+    vkey[v] = 0ull;
+  }
+}
+
+int crcw_tail(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, uint32_t first_round, uint32_t max_rounds,
+              uint32_t alive_small, uint32_t alive_large, CrcwTailOut* out) {
+  Workspace& w = g->ws;
+  cudaStream_t s = g->stream;
+  Launcher L;
+  hlm_b200_config as_crcw = *cfg;
+  as_crcw.variant = HLM_B200_VARIANT_CRCW;
+  ST_CHECK(setup_launcher(g, st, &as_crcw, max_rounds, L, nullptr, false));
+  const bool want_times = (cfg->flags & HLM_B200_FLAG_KERNEL_TIMES) != 0;
+  const bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact && !want_times;
+  if (use_graph && (!w.graph_exec[1] || !same_params(w.graph_key, L.P))) {
+    w.drop_graphs();
+    ST_CHECK(build_loop_graph(L, 1));
+  }
+  if (g->n) k_tail_vertices<<<grid_for(g, g->n), kBlock, 0, s>>>(w.dead, w.vtop, w.vkey, g->n);
+  ++L.launches;
+  Ctrl c;
+  std::memset(&c, 0, sizeof(c));
+  c.round = first_round;
+  c.parity = 0;  // the list of the previous round sits in buffer 0
+  c.count1[0] = alive_large;
+  c.active_prev = alive_small;
+  c.max_rounds = max_rounds;
+  CU_CHECK(cudaMemcpyAsync(w.ctrl, &c, sizeof(c), cudaMemcpyHostToDevice, s));
+  CrcwRunStats S;
+  ST_CHECK(crcw_run(g, L, max_rounds, use_graph, /*from_round1=*/false, want_times && !L.exact, c, S));
+  CU_CHECK(cudaGetLastError());
+  out->rounds_done = c.rounds_done;
+  out->limit = c.status == ST_ROUND_LIMIT;
+  out->tie_redo = S.tie_redo;
+  out->launches = L.launches + S.graph_kernels;
+  out->graph_launches = S.graph_launches;
+  out->t_filter = std::move(S.t_filter);
+  out->t_check = std::move(S.t_check);
+  return HLM_B200_OK;
 }
 
 static int ensure_pinned(Workspace& w, uint64_t total, bool need_w) {

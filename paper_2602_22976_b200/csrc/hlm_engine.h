@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "../../include/hlm_b200.h"
 #include "hlm_types.cuh"
 
@@ -142,6 +144,17 @@ bool reorder_enabled();
 bool renumber_enabled();
 int reorder_by_first_pin(Graph* g);
 bool crcw_is_faster(const Graph* g);
+// Rounds first_round.. of a matching on the CRCW kernels, continuing what the vertex-owned engine started
+// (hlm_crew2.inc hands over when few edges are left).  Expects in the workspace: seg_ids[0] / seg_cnt[0] =
+// the alive class-0 edges (ascending inside every region), large_state, dead = all covered vertices, and
+// mbits / mround / matched_cnt / deact_cnt of the rounds so far.
+struct CrcwTailOut {
+  uint32_t rounds_done = 0, tie_redo = 0, launches = 0, graph_launches = 0;
+  bool limit = false;
+  std::vector<float> t_filter, t_check;
+};
+int crcw_tail(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, uint32_t first_round, uint32_t max_rounds,
+              uint32_t alive_small, uint32_t alive_large, CrcwTailOut* out);
 // the rest of greedy_sorted as one ordered scan over the still-free edges (hlm_greedy.cu)
 int greedy_finish(Graph* g, uint32_t round, uint64_t* finished);
 int renumber_by_degree(Graph* g);

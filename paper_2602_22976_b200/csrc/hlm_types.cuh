@@ -37,6 +37,7 @@ enum LoopStatus : uint32_t {
   ST_ROUND_LIMIT = 2,
   ST_TIE = 3,    // a vertex saw two equal keys: redo this round on the exact path
   ST_EPOCH = 4,  // round tags wrapped: vkey must be cleared before continuing
+  ST_HANDOVER = 5,  // vertex-owned engine: few edges are left, the CRCW kernels finish the run
 };
 
 // Device-resident loop state.
