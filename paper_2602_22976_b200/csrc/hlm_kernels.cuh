@@ -991,7 +991,7 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
   uint32_t status = ST_RUNNING;
   c->ticket_f = 0;
   c->ticket_c = 0;
-  if (c->tie_flag) {
+  if (c->tie_flag && r <= c->max_rounds) {  // beyond the cap nothing commits: a tie seen by that sweep is moot
     status = ST_TIE;
   } else if (active == 0 && active_elsewhere == 0) {  // edge shards: other ranks may still be busy
     status = ST_DONE;  // loop condition of run_soft_delete (local_max_par.hpp:117)

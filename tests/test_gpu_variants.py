@@ -155,3 +155,55 @@ def test_auto_is_crcw_to_the_caller_on_either_engine(hb, port, ref, monkeypatch)
             assert got.report.work.total_edge_visits == theirs.edge_visits, f"{name} auto {forced}: edge visits"
             assert got.report.work.total_pin_visits == theirs.pin_visits, f"{name} auto {forced}: pin visits"
         dg.release()
+
+
+def test_vertex_owned_run_finished_by_the_crcw_kernels(hb, port, monkeypatch):
+    """variant auto on the vertex-owned engine hands the last rounds to the CRCW kernels once few edges are
+    alive (hlm_crew2.inc -> crcw_tail).  Forced early here (hand-over before round 3) on instances with
+    ragged and large edges, integer and real weights, and on streams whose ties send the tail's rounds
+    through the exact path: matching, rounds and per-round report must equal the oracle's."""
+    monkeypatch.setenv("HLM_B200_AUTO", "crew")
+    monkeypatch.setenv("HLM_B200_CREW_TAIL", "100000")  # percent of n alive pins: always true from round 2 on
+    cases = [
+        ("netlist", po.SYN_NETLIST, dict(n=60_000, m=120_000), True),
+        ("uniform", po.SYN_UNIFORM, dict(n=40_000, m=90_000, d=8), False),
+        ("powerlaw", po.SYN_POWERLAW, dict(n=50_000, m=100_000), False),
+    ]
+    streams = [po.Stream(seed=4), po.Stream(seed=4, noise_high=0.0), po.Stream(seed=8, kind=po.GEN_PARK_MILLER, noise_high=2.0 ** -50),
+               po.Stream(seed=2, mode=po.MODE_REPLACE_UNIFORM)]
+    for family, fam_id, kw, intw in cases:
+        g = port.syn_generate(fam_id, seed=6, int_weights=intw, **kw)
+        dg = hb.DeviceHypergraph.generate(family, seed=6, int_weights=intw, **kw)
+        for s in streams:
+            want = port.local_max(g, s)
+            for loop in ("graph", "host"):
+                got = dg.match(to_hb_stream(s), hb.ParallelConfig(variant="auto", loop_mode=loop))
+                assert_same_result(got, want, f"{family} tail {loop} {s}")
+                assert "crcw from round 3" in got.report.engine, got.report.engine
+            # the round cap hit inside the tail: partial matching and report of exactly 3 rounds
+            capped = port.local_max(g, s, max_rounds=3)
+            if capped.status == po.ROUND_LIMIT:
+                import pytest
+
+                with pytest.raises(hb.RoundLimitError) as ei:
+                    dg.match(to_hb_stream(s), hb.ParallelConfig(variant="auto", max_rounds=3))
+                assert list(ei.value.partial.matched_edges) == list(capped.matched_edges)
+                assert ei.value.report.deactivated_per_round == capped.per_round_deactivated
+        dg.release()
+
+
+def test_round_cap_with_ties_on_every_engine(hb, port):
+    """A tie seen by the sweep that follows the last allowed round must not commit anything (the sweep only counts
+    what that round deactivated): round cap + tie-prone streams on crcw, crew and auto."""
+    g = port.generate_random(4000, 9000, 2, 5, 12)
+    for s in (po.Stream(seed=5, noise_high=0.0), po.Stream(seed=5, kind=po.GEN_PARK_MILLER, noise_high=2.0 ** -50)):
+        for cap in (1, 2, 3):
+            want = port.local_max(g, s, max_rounds=cap)
+            if want.status != po.ROUND_LIMIT:
+                continue
+            for variant in ("crcw", "crew", "auto"):
+                with pytest.raises(hb.RoundLimitError) as ei:
+                    hb.run_variant(to_hb_graph(g), to_hb_stream(s), hb.ParallelConfig(variant=variant, max_rounds=cap))
+                assert list(ei.value.partial.matched_edges) == list(want.matched_edges), (variant, cap)
+                assert ei.value.report.matched_per_round_count == want.per_round_matched
+                assert ei.value.report.deactivated_per_round == want.per_round_deactivated
