@@ -118,6 +118,7 @@ struct CrewState {
   // ---- edge-partitioned runs (hlm_shard.inc) ----
   unsigned long long* lkey = nullptr;  // n: this shard's maximum at every live vertex (live-slot order)
   uint32_t* mnow = nullptr;            // m bits: matched in the round in progress, not yet committed
+  uint32_t* second = nullptr;          // m bits: the seconder of the edge named it in this round
   ShDevMem shdev;                      // the device's exchange arrays, when this is its first shard
 };
 
@@ -137,7 +138,7 @@ struct CrewParams {
   uint32_t* mbits;
   uint16_t* mround;
   uint32_t* counters;
-  uint32_t id_mask;  // incidence entries carry a first-pin flag in bit 31 when the instance has < 2^31 edges
+  uint32_t id_mask;  // incidence entries carry two role flags (bits 31, 30) when the instance has < 2^30 edges
 };
 
 template <typename T>
@@ -344,6 +345,7 @@ void crew_release(Graph* g) {
   std::free(c->graph_params);
   pool_free(c->lkey);
   pool_free(c->mnow);
+  pool_free(c->second);
   c->shdev.release();
   delete c;
   g->crew = nullptr;
@@ -400,7 +402,7 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
   P.stream.width = st->noise_high - st->noise_low;
   P.voff = reinterpret_cast<const unsigned long long*>(g->voff);
   P.vinc = g->vinc;
-  P.id_mask = g->vinc_flagged ? 0x7fffffffu : 0xffffffffu;
+  P.id_mask = g->vinc_flagged ? 0x3fffffffu : 0xffffffffu;
   P.wkey = c->wkey;
   P.estat = c->estat;
   P.top = c->top;
@@ -468,8 +470,8 @@ static int match_crew_soft(Graph* g, const hlm_b200_stream* st, const hlm_b200_c
 
 int match_crew(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out, int report_variant) {
   const char* env = std::getenv("HLM_B200_CREW_SOFT");
-  // the work-optimal form needs the first-pin flag of the incidence entries (bit 31: < 2^31 edges)
-  if ((env && env[0] == '1') || g->m >= 0x7fffffffu) return match_crew_soft(g, st, cfg, out, report_variant);
+  // the work-optimal form needs the two role flags of the incidence entries (bits 31, 30: < 2^30 edges)
+  if ((env && env[0] == '1') || g->m >= 0x3fffffffu) return match_crew_soft(g, st, cfg, out, report_variant);
   return match_crew_compacting(g, st, cfg, out, report_variant);
 }
 

@@ -177,11 +177,39 @@ __global__ void k_copy_u64(const unsigned long long* in, uint64_t count, unsigne
 }
 
 // pos[v] starts as voff[v]; the returning 64-bit add hands out the slots of v's list
-// flag_mode != 0: bit 31 of the entry written for ONE pin of every edge is set -- its proposer: the
-// vertex-owned matching kernels look at an edge only when the proposer names it as its argmax.
-// 1: the first pin; 2: the pin with the smallest vertex id, which on an instance renumbered by
-// descending degree is the pin with the most incident edges, i.e. the one least likely to name a
-// given edge (fewest proposals to check).
+// flag_mode != 0: two pins of every edge get a role, marked in the top bits of their entries -- bit 31 the
+// PROPOSER, bit 30 the SECONDER.  The vertex-owned matching kernels look at an edge (read its row from HBM)
+// only when the proposer names it as its argmax AND the seconder has said the same through a per-edge bit
+// that stays in L2.  1: the first and the second pin; 2: the pins with the smallest and second smallest
+// vertex ids, which on an instance renumbered by descending degree are the pins with the most incident
+// edges, i.e. the ones least likely to name a given edge (fewest proposals to check).  An edge with a
+// single pin plays both roles.
+__device__ __forceinline__ void inc_roles(const EdgeCsr& csr, uint64_t b, uint32_t s, int flag_mode, uint32_t& proposer,
+                                          uint32_t& seconder) {
+  proposer = 0u;
+  seconder = s > 1u ? 1u : 0u;
+  if (flag_mode != 2) return;
+  uint32_t best = 0xffffffffu, next = 0xffffffffu;
+  for (uint32_t i = 0; i < s; ++i) {
+    const uint32_t v = __ldg(csr.pins + b + i);
+    if (v < best) {
+      next = best;
+      seconder = proposer;
+      best = v;
+      proposer = i;
+    } else if (v < next) {
+      next = v;
+      seconder = i;
+    }
+  }
+  if (s == 1u) seconder = proposer;
+}
+
+__device__ __forceinline__ uint32_t inc_entry(uint32_t id, uint32_t i, uint32_t proposer, uint32_t seconder, int flag_mode) {
+  if (flag_mode == 0) return id;
+  return id | (i == proposer ? 0x80000000u : 0u) | (i == seconder ? 0x40000000u : 0u);
+}
+
 __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, uint32_t vhi, unsigned long long* pos,
                                  const uint32_t* orig, uint32_t* vinc, int flag_mode) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
@@ -189,23 +217,13 @@ __global__ void k_fill_incidence(const EdgeCsr csr, uint32_t m, uint32_t vlo, ui
     uint32_t s;
     csr.range(e, b, s);
     uint32_t id = 0xffffffffu;  // incidence lists name edges by the caller's ids
-    uint32_t proposer = 0;
-    if (flag_mode == 2) {
-      uint32_t best = 0xffffffffu;
-      for (uint32_t i = 0; i < s; ++i) {
-        const uint32_t v = __ldcs(csr.pins + b + i);
-        if (v < best) {
-          best = v;
-          proposer = i;
-        }
-      }
-      if (best < vlo || best >= vhi) proposer = 0xffffffffu;  // flagged by the pass that owns that vertex
-    }
+    uint32_t proposer = 0, seconder = 0;
+    inc_roles(csr, b, s, flag_mode, proposer, seconder);
     for (uint32_t i = 0; i < s; ++i) {
       const uint32_t v = __ldcs(csr.pins + b + i);
       if (v < vlo || v >= vhi) continue;
       if (id == 0xffffffffu) id = orig ? orig[e] : e;
-      vinc[atomicAdd(pos + v, 1ull)] = (flag_mode != 0 && i == proposer) ? (id | 0x80000000u) : id;
+      vinc[atomicAdd(pos + v, 1ull)] = inc_entry(id, i, proposer, seconder, flag_mode);
     }
   }
 }
@@ -226,19 +244,6 @@ __global__ void k_inc_bucket_cursors(const unsigned long long* voff, uint32_t n,
     const unsigned long long first = static_cast<unsigned long long>(b) << shift;
     bcur[b] = voff[first < n ? first : n];
   }
-}
-
-__device__ __forceinline__ uint32_t inc_proposer(const EdgeCsr& csr, uint64_t b, uint32_t s, int flag_mode) {
-  if (flag_mode != 2) return 0u;
-  uint32_t best = 0xffffffffu, at = 0u;
-  for (uint32_t i = 0; i < s; ++i) {
-    const uint32_t v = __ldg(csr.pins + b + i);
-    if (v < best) {
-      best = v;
-      at = i;
-    }
-  }
-  return at;
 }
 
 __global__ void __launch_bounds__(kBlock) k_inc_partition(const EdgeCsr csr, uint32_t m, const uint32_t* orig, uint32_t shift,
@@ -273,11 +278,12 @@ __global__ void __launch_bounds__(kBlock) k_inc_partition(const EdgeCsr csr, uin
       uint32_t s;
       csr.range(static_cast<uint32_t>(e), b, s);
       const uint32_t id = orig ? orig[e] : static_cast<uint32_t>(e);
-      const uint32_t proposer = inc_proposer(csr, b, s, flag_mode);
+      uint32_t proposer, seconder;
+      inc_roles(csr, b, s, flag_mode, proposer, seconder);
       for (uint32_t i = 0; i < s; ++i) {
         const uint32_t v = __ldg(csr.pins + b + i);
         const uint32_t bk = v >> shift;
-        const uint32_t raw = (flag_mode != 0 && i == proposer) ? (id | 0x80000000u) : id;
+        const uint32_t raw = inc_entry(id, i, proposer, seconder, flag_mode);
         pairs[s_base[bk] + atomicAdd(s_cnt + bk, 1u)] = (static_cast<unsigned long long>(v) << 32) | raw;
       }
     }
@@ -410,7 +416,7 @@ int build_incidence(Graph* g) {
   ST_CHECK(dalloc(&g->vinc, g->kappa + 16));  // padding: the vertex-owned sweep copies windows that end on a multiple of 16 entries
   g->device_bytes += (static_cast<uint64_t>(g->n) + 1) * 8 + g->kappa * 4;
   CU_CHECK(cudaMemsetAsync(g->vinc + g->kappa, 0xff, 64, g->stream));
-  g->vinc_flagged = g->m < 0x7fffffffu;
+  g->vinc_flagged = g->m < 0x3fffffffu;  // two role bits per entry
   // proposer of an edge: its highest-degree pin where vertex ids are degree ranks (renumbered, ragged
   // instances: an order of magnitude fewer proposals on skewed degrees), else its first pin
   g->vinc_first_pin = !(g->vold && !g->uniform_d) || std::getenv("HLM_B200_PROPOSER_FIRST") != nullptr;
