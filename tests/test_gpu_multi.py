@@ -119,6 +119,23 @@ def test_host_arrays_over_several_gpus(hb, port):
         _release(shards)
 
 
+def test_sharded_call_rejects_what_it_cannot_do(hb, port):
+    from paper_2602_22976_b200 import multi_gpu
+
+    shards = multi_gpu.generate_shards("uniform", 2, n=2000, m=5000, d=3, seed=1)
+    with pytest.raises(NotImplementedError):
+        multi_gpu.match_sharded(shards, hb.WeightStream(), hb.ParallelConfig(variant="greedy"))
+    with pytest.raises(hb.InputError):
+        multi_gpu.match_sharded(shards, hb.WeightStream(noise_low=2.0, noise_high=1.0))
+    with pytest.raises(hb.InputError):  # shards of different instances
+        other = multi_gpu.generate_shards("uniform", 2, n=3000, m=5000, d=3, seed=1)
+        multi_gpu.match_sharded([shards[0], other[1]], hb.WeightStream())
+    whole = hb.DeviceHypergraph.generate("powerlaw", n=3000, m=6000, seed=1)  # loaded whole: vertices renumbered
+    with pytest.raises(hb.InputError):
+        multi_gpu.match_sharded([whole, shards[1]], hb.WeightStream())
+    _release(shards + other + [whole])
+
+
 def test_two_real_ranks_when_two_gpus_are_visible(hb, port, tmp_path):
     """Two processes, two GPUs, NCCL between them; skipped on a one-GPU box."""
     from paper_2602_22976_b200 import _lib
