@@ -530,9 +530,18 @@ struct PinStager {
     }
     return a.type == cudaMemoryTypeUnregistered;
   }
+  // the ring is one per process: a second loader running at the same time (another thread, another handle)
+  // takes the plain copy path instead of sharing the slots
+  static std::mutex& ring_mutex() {
+    static std::mutex mu;
+    return mu;
+  }
+  bool locked = false;
   bool init(const void* from, void* to, size_t n) {
     ring = ring_memory();
     if (!ring) return false;
+    if (!ring_mutex().try_lock()) return false;
+    locked = true;
     if (const char* cenv = std::getenv("HLM_B200_STAGE_CHUNK_KB")) kChunkBytes = std::max<size_t>(64, std::strtoull(cenv, nullptr, 10)) << 10;
     if (const char* senv = std::getenv("HLM_B200_STAGE_SLOTS")) kSlots = std::strtoull(senv, nullptr, 10);
     kChunkBytes = std::min(kChunkBytes, kRingBytes / 2) & ~static_cast<size_t>(63);
@@ -551,6 +560,7 @@ struct PinStager {
   ~PinStager() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (locked) ring_mutex().unlock();
   }
   // worker side: fill one chunk if a slot is free.  0 = nothing left, 1 = filled one, 2 = ring full
   int fill_one() {

@@ -51,6 +51,21 @@ def main():
                   "sweep_bytes_per_launch": None,
                   "source": "ncu --set full --clock-control none -k regex:k_c2_argmax_light|k_c2_check|k_c2_kill_light -c 9 python "
                             "scripts/crew_ncu_target.py u8 (profiles/ncu_crew_u8_r02.md): rounds 1-3"}
+    import os
+    for name, lists_bytes in (("c3", 594_701_884 * 4), ("c4", 90_191_885 * 4)):
+        rep = f"gpurun_out/crew_{name}_r02.ncu-rep"
+        if not os.path.exists(rep):
+            continue
+        ks = raw(rep)
+        arg = [k for k in ks if "k_c2_argmax" in k["kernel"] and k["ns"] > 2e4]
+        r1 = [k for k in arg if "<0," in k["kernel"]]
+        out[name] = {"kernel": "k_c2_argmax_light / k_c2_argmax_task <MODE,KM>", "launches_captured": len(arg),
+                     "per_launch": [round(k["read"] + k["write"]) for k in arg],
+                     "list_bytes_round1": lists_bytes,
+                     "round1_dram_over_list_bytes": sum(k["read"] + k["write"] for k in r1) / lists_bytes if r1 else None,
+                     "sweep_bytes_per_launch": None,
+                     "source": f"ncu --set full --clock-control none -k regex:k_c2_argmax_light|k_c2_argmax_task|k_c2_check|k_c2_kill_light "
+                               f"-c 12 python scripts/crew_ncu_target.py {name} (profiles/ncu_crew_{name}_r02.md): rounds 1-2"}
     json.dump(out, open("profiles/traffic_r02.json", "w"), indent=1)
     print(json.dumps(out, indent=1))
 
