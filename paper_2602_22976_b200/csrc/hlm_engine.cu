@@ -175,6 +175,12 @@ void* host_result_alloc(size_t bytes) {
   return std::malloc(bytes);
 }
 
+// true when `p` came from the page-locked pool (the device can write to it directly)
+static bool host_result_pinned(const void* p) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  return g_host_live.find(const_cast<void*>(p)) != g_host_live.end();
+}
+
 void host_result_free(void* p) {
   if (!p) return;
   HostBlock drop = {nullptr, 0};
@@ -224,6 +230,9 @@ void Workspace::release() {
   dev_free(out_round);
   dev_free(out_w);
   dev_free(int_sum);
+  dev_free(fused_block_cnt);
+  dev_free(fused_block_isum);
+  if (fused_sum) cudaFreeHost(fused_sum);
   if (pin_w) cudaFreeHost(pin_w);
   drop_graphs();
   if (ev0) cudaEventDestroy(ev0);
@@ -862,8 +871,10 @@ int ensure_workspace(Graph* g, uint32_t max_rounds) {
     // class-0 lists: one region of seg_cap edge ids per warp, a CTA claims 8 regions at a time;
     // several claims per resident CTA so the ticket scheduler can balance uneven survivor counts
     const uint32_t target = static_cast<uint32_t>(g->num_sms) * 64u * kWarpsPerBlock;
-    w.seg_cap = std::max<uint32_t>(128u, (g->m + target - 1) / std::max(1u, target));
-    w.seg_cap = (w.seg_cap + 63u) / 64u * 64u;
+    uint32_t seg_min = 128u;
+    if (const char* env = std::getenv("HLM_B200_SEG_MIN")) seg_min = std::max(32, std::atoi(env)) / 32u * 32u;
+    w.seg_cap = std::max<uint32_t>(seg_min, (g->m + target - 1) / std::max(1u, target));
+    w.seg_cap = (w.seg_cap + 31u) / 32u * 32u;
     w.nseg = std::max<uint32_t>(1u, (g->m + w.seg_cap - 1) / w.seg_cap);
     w.nseg = (w.nseg + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
     for (int b = 0; b < 2; ++b) {
@@ -1246,7 +1257,129 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   return HLM_B200_OK;
 }
 
+// Small uniform instances run all their rounds in one cooperative launch (k_rounds_fused) instead of the
+// CUDA graph: below ~8 M pins the three launches per round cost more than the round.  The limit is the pin
+// count of the whole instance (HLM_B200_FUSED_MAX_PINS overrides it; 0 disables the fused loop).
+static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
+  if (L.exact || g->num_large) return false;
+  if (g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
+  uint64_t limit = 1ull << 23;
+  if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) limit = std::strtoull(env, nullptr, 10);
+  return g->kappa <= limit;
+}
+
+static bool fused_pipelined(const Graph* g) {
+  if (const char* env = std::getenv("HLM_B200_FUSED_PIPE")) return env[0] == '1';
+  return g->uniform_d == 8;  // measured (scripts/fused_tune.sh): d = 8 gains 11 %, d = 2, 4 lose 5-10 %
+}
+
+static const void* fused_kernel(const Graph* g) {
+  if (fused_pipelined(g)) {
+    switch (g->uniform_d) {
+      case 2: return reinterpret_cast<const void*>(&k_rounds_fused<2, true>);
+      case 4: return reinterpret_cast<const void*>(&k_rounds_fused<4, true>);
+      default: return reinterpret_cast<const void*>(&k_rounds_fused<8, true>);
+    }
+  }
+  switch (g->uniform_d) {
+    case 2: return reinterpret_cast<const void*>(&k_rounds_fused<2, false>);
+    case 4: return reinterpret_cast<const void*>(&k_rounds_fused<4, false>);
+    default: return reinterpret_cast<const void*>(&k_rounds_fused<8, false>);
+  }
+}
+
+// the cooperative grid: what is resident at once (at most 4 CTAs per SM; HLM_B200_FUSED_CTAS lowers it)
+static int fused_grid_size(Graph* g, const void* fn) {
+  if (g->fused_grid) return HLM_B200_OK;
+  int occ = 0;
+  CU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0));
+  if (occ < 1) {
+    set_error("internal: the fused round kernel does not fit on an SM");
+    return HLM_B200_ERR_CUDA;
+  }
+  int per_sm = std::min(occ, 4);
+  if (const char* env = std::getenv("HLM_B200_FUSED_CTAS")) per_sm = std::max(1, std::min(occ, std::atoi(env)));
+  g->fused_grid = g->num_sms * per_sm;
+  return HLM_B200_OK;
+}
+
+static int launch_fused_rounds(Graph* g, Launcher& L, const FusedExtra* extra) {
+  RoundParams P = L.P;
+  FusedExtra X;
+  if (extra) X = *extra;
+  else std::memset(&X, 0, sizeof(X));
+  // (the hot windows stay: ld.ca lines cannot outlive a phase, every grid barrier ends with CCTL.IVALL)
+  if (std::getenv("HLM_B200_FUSED_NO_L1")) P.hot_vtop = P.hot_bits = 0u;
+  const void* fn = fused_kernel(g);
+  ST_CHECK(fused_grid_size(g, fn));
+  void* args[] = {&P, &X};
+  CU_CHECK(cudaLaunchCooperativeKernel(fn, dim3(g->fused_grid), dim3(kBlock), args, 0, g->stream));
+  ++L.launches;
+  return HLM_B200_OK;
+}
+
+static bool integer_weight_sum(const Graph* g) {
+  // integer weights: every partial sum is an integer below 2^53, so any summation order gives
+  // the reference's ascending-id sum exactly and the device can reduce in parallel
+  return g->base && g->base_integral && g->base_max * static_cast<double>(g->m) < 9007199254740992.0;
+}
+
+// Small instance, whole matching in one launch: buffers of the assembly phase and the caller's (page-locked)
+// result arrays, sized by the largest matching the instance can have.  *ok = false: use the usual sequence.
+static int fused_prepare(Graph* g, const hlm_b200_config* cfg, const Ctrl& c0, FusedExtra* fx, PreAssembled* pre, bool* ok) {
+  Workspace& w = g->ws;
+  *ok = false;
+  if (g->base && !integer_weight_sum(g)) return HLM_B200_OK;  // ordered FP64 sum on the host: usual path
+  if (std::getenv("HLM_B200_NO_FUSED_RESULT")) return HLM_B200_OK;
+  ST_CHECK(fused_grid_size(g, fused_kernel(g)));
+  if (!w.fused_block_cnt) {
+    ST_CHECK(dev_alloc(&w.fused_block_cnt, static_cast<size_t>(g->fused_grid), g));
+    ST_CHECK(dev_alloc(&w.fused_block_isum, static_cast<size_t>(g->fused_grid), g));
+  }
+  if (!w.fused_sum) CU_CHECK(cudaHostAlloc(&w.fused_sum, sizeof(FusedSummary), cudaHostAllocDefault));
+  const uint64_t bound = std::min<uint64_t>(g->m, g->n / g->uniform_d);  // matched edges are disjoint
+  const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
+  if (bound + 8 > w.out_cap) {  // device staging of the result (shared with the usual assembly)
+    dev_free(w.out_ids);
+    dev_free(w.out_round);
+    dev_free(w.out_w);
+    w.out_ids = nullptr;
+    w.out_round = nullptr;
+    w.out_w = nullptr;
+    w.out_cap = bound + 8;
+    ST_CHECK(dev_alloc(&w.out_ids, w.out_cap, g));
+    ST_CHECK(dev_alloc(&w.out_round, w.out_cap, g));
+  }
+  pre->ids = static_cast<uint32_t*>(host_result_alloc(sizeof(uint32_t) * (bound + 4)));
+  pre->round = want_round ? static_cast<uint16_t*>(host_result_alloc(sizeof(uint16_t) * (bound + 8))) : nullptr;
+  if (!pre->ids || !host_result_pinned(pre->ids) || (want_round && (!pre->round || !host_result_pinned(pre->round)))) {
+    host_result_free(pre->ids);
+    host_result_free(pre->round);
+    pre->ids = nullptr;
+    pre->round = nullptr;
+    return HLM_B200_OK;
+  }
+  pre->sum = w.fused_sum;
+  w.fused_sum->assembled = 0u;
+  fx->c0 = c0;
+  fx->init = 1u;
+  fx->rounds_cap = w.rounds_cap;
+  fx->mbits_words = w.mbits_words;
+  fx->out_cap = static_cast<uint32_t>(bound);
+  fx->block_cnt = w.fused_block_cnt;
+  fx->block_isum = w.fused_block_isum;
+  fx->dev_ids = w.out_ids;
+  fx->dev_round = w.out_round;
+  fx->out_ids = pre->ids;
+  fx->out_round = pre->round;
+  fx->base_int = integer_weight_sum(g) ? g->base : nullptr;
+  fx->sum = w.fused_sum;
+  *ok = true;
+  return HLM_B200_OK;
+}
+
 struct CrcwRunStats {
+  FusedExtra* fused = nullptr;  // small instances: the fused kernel also initialises and assembles (match_crcw)
   uint32_t tie_redo = 0, graph_launches = 0, graph_kernels = 0;
   std::vector<float> t_filter, t_check;  // per round, host loop with want_times
 };
@@ -1271,7 +1404,29 @@ static int crcw_run(Graph* g, Launcher& L, uint32_t max_rounds, bool use_graph, 
   std::vector<float>& t_check = S.t_check;
   {
     for (;;) {
-      if (use_graph) {
+      bool have_ctrl = false;
+      if (use_graph && fused_rounds_ok(g, L)) {
+        ST_CHECK(launch_fused_rounds(g, L, S.fused));
+        ++graph_launches;
+        if (S.fused) {
+          S.fused->init = 0u;  // a relaunch (after a tie or a tag wrap) continues the run
+          if (S.fused->sum) {  // the kernel leaves the control block in page-locked memory: no copy, one sync
+            CU_CHECK(cudaEventRecord(w.ev1, s));
+            CU_CHECK(cudaStreamSynchronize(s));
+            c = S.fused->sum->ctrl;
+            have_ctrl = true;
+#ifdef HLM_FUSED_TRACE
+            if (std::getenv("HLM_B200_TRACE")) {
+              const unsigned long long* t = S.fused->sum->trace;
+              std::fprintf(stderr, "[hlm_b200] fused phases (us):");
+              for (int i = 1; i < 64 && t[i] >= t[i - 1] && t[i]; ++i) std::fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
+              std::fprintf(stderr, "\n");
+              std::memset(S.fused->sum->trace, 0, sizeof(S.fused->sum->trace));
+            }
+#endif
+          }
+        }
+      } else if (use_graph) {
         // one launch runs every round; it only comes back early for a tie or a tag wrap, and the
         // run is then resumed with the WHILE node alone (the full graph starts at round 1)
         const int which = (from_round1 && graph_launches == 0) ? 0 : 1;
@@ -1295,8 +1450,10 @@ static int crcw_run(Graph* g, Launcher& L, uint32_t max_rounds, bool use_graph, 
         if (want_times) CU_CHECK(cudaEventRecord(tev[2], s));
         L.advance(s, 0, 0);
       }
-      CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
-      CU_CHECK(cudaStreamSynchronize(s));
+      if (!have_ctrl) {
+        CU_CHECK(cudaMemcpyAsync(&c, w.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_CHECK(cudaStreamSynchronize(s));
+      }
       if (in_graph) {
         in_graph = false;
         // sweeps executed by this launch: rounds c_before.round .. last, where the last sweep is
@@ -1384,17 +1541,27 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   c0.count1[0] = g->num_large;
   c0.active_prev = g->m;
   c0.max_rounds = max_rounds;
-  CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
-  CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
-  CU_CHECK(cudaMemsetAsync(w.vtop, 0, static_cast<size_t>(g->n) * 4, s));
-  CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
-  CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
-  CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
-  CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
-  if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
+  // a small uniform instance: ONE cooperative launch zeroes the state, runs every round and writes the
+  // result into the caller's page-locked arrays (k_rounds_fused); everything else: the usual sequence
+  FusedExtra fx;
+  PreAssembled pre;
+  bool fused_all = false;
+  std::memset(&fx, 0, sizeof(fx));
+  if (use_graph && g->m && !greedy && fused_rounds_ok(g, L)) ST_CHECK(fused_prepare(g, cfg, c0, &fx, &pre, &fused_all));
+  if (!fused_all) {
+    CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+    CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+    CU_CHECK(cudaMemsetAsync(w.vtop, 0, static_cast<size_t>(g->n) * 4, s));
+    CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
+    CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
+    CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+    CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+    if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
+  }
 
   Ctrl c = c0;
   CrcwRunStats S;
+  if (fused_all) S.fused = &fx;
   const bool want_times = (cfg->flags & HLM_B200_FLAG_KERNEL_TIMES) && !use_graph && !L.exact;
   if (g->m == 0)
     c.status = ST_DONE;
@@ -1429,7 +1596,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
     c.status = ST_DONE;
     tr.mark("match: greedy tail");
   }
-  int rc = assemble_result(g, rounds, cfg, cfg->variant, out);
+  int rc = assemble_result(g, rounds, cfg, cfg->variant, out, 0.0, fused_all ? &pre : nullptr);
   tr.mark("match: result");
   if (rc != HLM_B200_OK) return rc;
   if (c.status == ST_ROUND_LIMIT && requested > max_rounds) {
@@ -1495,12 +1662,20 @@ static int ensure_pinned(Workspace& w, uint64_t total, bool need_w) {
 // finish_matching (local_max_seq.hpp:74-83) + the RunReport counters.  Expects the matched
 // bitmap (ws.mbits) and the per-edge round record (ws.mround) to be final.
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
-                    hlm_b200_result* out, double weight_before) {
+                    hlm_b200_result* out, double weight_before, const PreAssembled* pre) {
   Workspace& w = g->ws;
   cudaStream_t s = g->stream;
   const uint32_t m = g->m;
   uint64_t total = 0;
-  if (m) {
+  // the fused kernel of a small instance may have done all of it already (ids, rounds, counters, weight sum)
+  const bool done = pre && pre->sum && pre->sum->assembled && pre->sum->ctrl.rounds_done == rounds;
+  if (pre && !done) {
+    host_result_free(pre->ids);
+    host_result_free(pre->round);
+  }
+  if (done) {
+    total = pre->sum->total;
+  } else if (m) {
     k_assemble_count<<<w.num_chunks, kBlock, 0, s>>>(w.mbits, w.mbits_words, w.chunk_cnt);
     k_scan_small<<<1, 1024, 0, s>>>(w.chunk_cnt, w.num_chunks, w.scan_total);
     CU_CHECK(cudaMemcpyAsync(&total, w.scan_total, 8, cudaMemcpyDeviceToHost, s));
@@ -1510,8 +1685,7 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
   // integer weights: every partial sum is an integer below 2^53, so any summation order gives
   // the reference's ascending-id sum exactly and the device can reduce in parallel
-  const bool int_sum = g->base && g->base_integral &&
-                       g->base_max * static_cast<double>(m) < 9007199254740992.0;
+  const bool int_sum = integer_weight_sum(g);
   const bool need_w = g->base != nullptr && !int_sum;
   if (total > w.out_cap || (need_w && !w.out_w)) {
     dev_free(w.out_ids);
@@ -1528,8 +1702,13 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
   ST_CHECK(ensure_pinned(w, total, need_w));
   out->num_matched = total;
   out->rounds = rounds;
-  out->matched_edges = static_cast<uint32_t*>(host_result_alloc(sizeof(uint32_t) * (total + 1)));
-  out->matched_round = want_round ? static_cast<uint16_t*>(host_result_alloc(sizeof(uint16_t) * (total + 1))) : nullptr;
+  if (done) {
+    out->matched_edges = pre->ids;
+    out->matched_round = pre->round;
+  } else {
+    out->matched_edges = static_cast<uint32_t*>(host_result_alloc(sizeof(uint32_t) * (total + 1)));
+    out->matched_round = want_round ? static_cast<uint16_t*>(host_result_alloc(sizeof(uint16_t) * (total + 1))) : nullptr;
+  }
   out->per_round_matched = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
   out->per_round_deactivated = static_cast<uint32_t*>(std::calloc(rounds + 1, sizeof(uint32_t)));
   if (!out->matched_edges || !out->per_round_matched || !out->per_round_deactivated ||
@@ -1538,7 +1717,13 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     return HLM_B200_ERR_NOMEM;
   }
   unsigned long long isum = 0;
-  if (total) {
+  if (done) {
+    isum = pre->sum->isum;
+    for (uint32_t q = 0; q < rounds; ++q) {
+      out->per_round_matched[q] = pre->sum->matched[q + 1];
+      out->per_round_deactivated[q] = pre->sum->dropped[q + 1];
+    }
+  } else if (total) {
     if (int_sum) CU_CHECK(cudaMemsetAsync(w.int_sum, 0, 8, s));
     k_assemble_write<<<w.num_chunks, kBlock, 0, s>>>(
         w.mbits, w.mbits_words, w.chunk_cnt, w.mround, g->base, g->id_base, w.out_ids,
@@ -1550,12 +1735,14 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
     if (need_w) CU_CHECK(cudaMemcpyAsync(w.pin_w, w.out_w, total * 8, cudaMemcpyDeviceToHost, s));
     if (int_sum) CU_CHECK(cudaMemcpyAsync(&isum, w.int_sum, 8, cudaMemcpyDeviceToHost, s));
   }
-  if (rounds) {
+  if (rounds && !done) {
     CU_CHECK(cudaMemcpyAsync(out->per_round_matched, w.matched_cnt + 1, rounds * 4ull, cudaMemcpyDeviceToHost, s));
     CU_CHECK(cudaMemcpyAsync(out->per_round_deactivated, w.deact_cnt + 1, rounds * 4ull, cudaMemcpyDeviceToHost, s));
   }
-  CU_CHECK(cudaEventRecord(w.ev1, s));
-  CU_CHECK(cudaStreamSynchronize(s));
+  if (!done) {  // (done: the event follows the fused launch and the stream is idle)
+    CU_CHECK(cudaEventRecord(w.ev1, s));
+    CU_CHECK(cudaStreamSynchronize(s));
+  }
   // the device counts every edge dropped from the active list; the reference's "deactivated"
   // excludes the ones that matched (local_max_par.hpp:166-168)
   for (uint32_t q = 0; q < rounds; ++q) out->per_round_deactivated[q] -= out->per_round_matched[q];

@@ -60,6 +60,10 @@ struct Workspace {
   uint32_t graph_body_launches = 0;  // one iteration of the WHILE body
   uint32_t launches = 0;
   unsigned long long pins_matched = 0;  // ragged instances: pins of the matched edges of the last run
+  // one-launch matching of small instances (k_rounds_fused)
+  uint32_t* fused_block_cnt = nullptr;
+  unsigned long long* fused_block_isum = nullptr;
+  hlmb::FusedSummary* fused_sum = nullptr;  // page-locked host memory
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void drop_graphs();
   void release();
@@ -115,7 +119,7 @@ struct Graph {
   bool vinc_first_pin = true;  // the proposer is the edge's first pin (else: its pin with the smallest vertex id)
   uint64_t device_bytes = 0;
   uint64_t h2d_bytes = 0;
-  int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0;
+  int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0, fused_grid = 0;
   Workspace ws;
   CrewState* crew = nullptr;
   EdgeCsr csr() const;
@@ -169,8 +173,14 @@ void crew_release(Graph* g);
 struct Comm;  // hlm_comm.h
 int match_sharded(Graph* const* graphs, int num_shards, Comm* comm, const hlm_b200_stream* st, const hlm_b200_config* cfg,
                   hlm_b200_result* results, hlm_b200_shard_report* report);
+// result arrays the fused kernel filled before assemble_result runs (page-locked, from host_result_alloc)
+struct PreAssembled {
+  const hlmb::FusedSummary* sum = nullptr;
+  uint32_t* ids = nullptr;
+  uint16_t* round = nullptr;
+};
 int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int variant,
-                    hlm_b200_result* out, double weight_before = 0.0);
+                    hlm_b200_result* out, double weight_before = 0.0, const PreAssembled* pre = nullptr);
 int device_exclusive_scan_u32_to_u64(Graph* g, const uint32_t* in, uint64_t* out, uint64_t count,
                                      uint64_t* total);
 

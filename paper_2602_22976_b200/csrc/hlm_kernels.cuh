@@ -2,6 +2,8 @@
 // tie path, loader helpers, result assembly and verification.  Included by hlm_engine.cu only.
 // Kernel roles and the reference phases they replace: see hlm_types.cuh and DESIGN.md.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "hlm_types.cuh"
 
 namespace hlmb {
@@ -28,7 +30,7 @@ namespace hlmb {
 
 __device__ __forceinline__ uint32_t region_count(const RoundParams& P, bool ident, const uint32_t* cnt,
                                                  uint32_t seg) {
-  if (!ident) return cnt[seg];
+  if (!ident) return __ldcg(cnt + seg);  // written by the previous sweep (same launch in the fused kernel)
   const uint64_t b = static_cast<uint64_t>(seg) * P.seg_cap;
   return b >= P.m ? 0u : static_cast<uint32_t>(min(static_cast<uint64_t>(P.seg_cap), P.m - b));
 }
@@ -248,10 +250,12 @@ struct SweepTuning {  // CTAs per SM = register budget of the four in-flight bat
   static constexpr int kMinBlocks = D == 2 ? HLM_SWEEP_MIN_BLOCKS : (D == 4 ? HLM_SWEEP_MIN_BLOCKS_D4 : HLM_SWEEP_MIN_BLOCKS_D8);
 };
 
-template <int D, bool VMAX, bool R1>
-__global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_uniform(const RoundParams P) {
+// STRIDED: regions are dealt out by warp index (warp, warp + grid warps, ...) instead of by ticket -- the
+// fused kernel of small instances, where thousands of same-address ticket atomics (one per ns) would cost
+// more than the sweep
+template <int D, bool VMAX, bool R1, bool STRIDED = false>
+__device__ __forceinline__ void sweep_uniform_body(const RoundParams& P, DepositQueue* s_queue) {
   static_assert(!R1 || VMAX, "round 1 without keys has nothing to do");
-  __shared__ DepositQueue s_queue[SweepCtx<D, VMAX, R1>::kQueue ? kWarpsPerBlock : 1];
   Ctrl* c = P.ctrl;
   const uint32_t par = c->parity;
   SweepCtx<D, VMAX, R1> X{P};
@@ -275,9 +279,15 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   st.tie = false;
 
   const uint32_t gran = R1 ? 1u : claim_granularity(P, c->active_prev);
+  uint32_t next_claim = grid_warp();
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, X.lane, false) * gran;
+      if constexpr (STRIDED) {
+        seg = next_claim * gran;
+        next_claim += gridDim.x * kWarpsPerBlock;
+      } else {
+        seg = claim_region(&c->ticket_f, X.lane, false) * gran;
+      }
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -322,10 +332,16 @@ __global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_un
   if (st.tie) c->tie_flag = 1u;
 }
 
+template <int D, bool VMAX, bool R1>
+__global__ void __launch_bounds__(kBlock, SweepTuning<D>::kMinBlocks) k_sweep_uniform(const RoundParams P) {
+  __shared__ DepositQueue s_queue[SweepCtx<D, VMAX, R1>::kQueue ? kWarpsPerBlock : 1];
+  sweep_uniform_body<D, VMAX, R1>(P, s_queue);
+}
+
 // Non-pipelined form of the same sweep: one batch per warp at a time, 32 registers, 64 resident
 // warps per SM.  Latency is hidden by occupancy instead of by the per-warp pipeline.
-template <int D, bool VMAX>
-__global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform_simple(const RoundParams P) {
+template <int D, bool VMAX, bool STRIDED = false>
+__device__ __forceinline__ void sweep_uniform_simple_body(const RoundParams& P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -343,9 +359,15 @@ __global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform
   uint32_t local_deact = 0, local_kept = 0;
   bool tie = false;
   const uint32_t gran = claim_granularity(P, c->active_prev);
+  uint32_t next_claim = grid_warp();
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, lane, false) * gran;
+      if constexpr (STRIDED) {
+        seg = next_claim * gran;
+        next_claim += gridDim.x * kWarpsPerBlock;
+      } else {
+        seg = claim_region(&c->ticket_f, lane, false) * gran;
+      }
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -435,6 +457,138 @@ __global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform
     if (local_kept) atomicAdd(&c->active_small, local_kept);
   }
   if (tie) c->tie_flag = 1u;
+}
+
+// The sweep of the fused small-instance kernel: the same decisions as the plain sweep, ITEMS batches of a
+// region per step with the loads of all of them issued together.  A small instance is latency-bound -- the
+// resident warps each walk a few batches one dependent L2 round trip after the other (config 1: 6.6 batches
+// per warp, ~5 trips each) -- so the trips of ITEMS batches overlap.  Regions by warp index (no tickets);
+// deactivation always on the dead bitmap (identical to the kTopDead test: mark_dead sets both).
+template <int D, int ITEMS>
+__device__ __forceinline__ void sweep_uniform_ilp_body(const RoundParams& P) {
+  Ctrl* c = P.ctrl;
+  const uint32_t r = c->round;
+  const uint32_t par = c->parity;
+  const bool in_ident = r <= 2;
+  const bool out_ident = r == 1;
+  const bool peek = r > 1 || P.ks.precheck;
+  const uint32_t* in = P.seg_ids[par];
+  const uint32_t* in_cnt = P.seg_cnt[par];
+  uint32_t* out = P.seg_ids[par ^ 1];
+  uint32_t* out_cnt = P.seg_cnt[par ^ 1];
+  const uint32_t tag = round_tag(P.ks, r);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t local_deact = 0, local_kept = 0;
+  bool tie = false;
+  const uint32_t gran = claim_granularity(P, c->active_prev);
+  const uint32_t stride = gridDim.x * kWarpsPerBlock * gran;
+  for (uint32_t first = grid_warp() * gran; first < P.nseg; first += stride) {
+    const uint32_t last = min(P.nseg, first + gran);
+    for (uint32_t seg = first; seg < last; ++seg) {
+      const uint32_t cnt = region_count(P, in_ident, in_cnt, seg);
+      const uint32_t seg_base = seg * P.seg_cap;
+      uint32_t out_off = 0, cand_off = 0;
+      if (r == 2 && cnt && span_all_dead(P, seg_base, cnt, lane)) {
+        if (lane == 0) {
+          out_cnt[seg] = 0;
+          P.cand_cnt[seg] = 0;
+          local_deact += cnt;
+        }
+        continue;
+      }
+      for (uint32_t t0 = 0; t0 < cnt; t0 += 32u * ITEMS) {
+        uint32_t e[ITEMS];
+        bool live[ITEMS], cand[ITEMS];
+        PinVec<D> pv[ITEMS];
+        uint32_t cur[ITEMS][D];
+        unsigned long long key[ITEMS];
+        // every load below is unconditional (lanes past the end read the region's first edge): no branch
+        // separates the loads of the ITEMS batches
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t idx = t0 + k * 32u + lane;
+          live[k] = idx < cnt;
+          const uint32_t pos = seg_base + (live[k] ? idx : 0u);
+          e[k] = in_ident ? pos : __ldcs(in + pos);
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) pv[k] = load_pins_stream<D>(P.csr.pins, e[k]);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+#pragma unroll
+          for (int i = 0; i < D; ++i) cur[k][i] = 0u;
+        if (peek) {
+          bool dead_any[ITEMS];
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k) {
+            dead_any[k] = false;
+#pragma unroll
+            for (int i = 0; i < D; ++i) dead_any[k] |= is_dead(P, pv[k].v[i]);
+          }
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k)
+            if (live[k] && dead_any[k]) {
+              live[k] = false;
+              ++local_deact;
+            }
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k)
+            if (live[k]) {
+#pragma unroll
+              for (int i = 0; i < D; ++i) cur[k][i] = ld_top(P, pv[k].v[i]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          key[k] = 0ull;
+          if (live[k]) key[k] = priority_key(P.stream, P.ks, edge_gid(P, e[k]), r, base_of(P, e[k]), tag);
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          cand[k] = false;
+          if (live[k]) {
+            const uint32_t hi = static_cast<uint32_t>(key[k] >> 32);
+            bool lost = false;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              tie |= deposit_key(P, pv[k].v[i], key[k], cur[k][i]);
+              lost |= cur[k][i] > hi;
+            }
+            cand[k] = !lost;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {  // batches in list order
+          if (!out_ident) {
+            const uint32_t ballot = __ballot_sync(0xffffffffu, live[k]);
+            if (live[k]) __stcs(out + seg_base + out_off + __popc(ballot & lt_mask), e[k]);
+            out_off += __popc(ballot);
+          }
+          const uint32_t ballot = __ballot_sync(0xffffffffu, cand[k]);
+          if (cand[k]) P.cand_ids[seg_base + cand_off + __popc(ballot & lt_mask)] = e[k];
+          cand_off += __popc(ballot);
+        }
+      }
+      if (lane == 0) {
+        const uint32_t kept = out_ident ? cnt : out_off;
+        out_cnt[seg] = kept;
+        P.cand_cnt[seg] = cand_off;
+        local_kept += kept;
+      }
+    }
+  }
+  const uint32_t d = warp_sum(local_deact);
+  if (lane == 0) {
+    if (d) atomicAdd(P.deact_cnt + (r - 1), d);
+    if (local_kept) atomicAdd(&c->active_small, local_kept);
+  }
+  if (tie) c->tie_flag = 1u;
+}
+
+template <int D, bool VMAX>
+__global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform_simple(const RoundParams P) {
+  sweep_uniform_simple_body<D, VMAX>(P);
 }
 
 // The same sweep with the survivors processed densely: three quarters of the edges a later round
@@ -727,8 +881,8 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
 // list id -> pins -> filter word are in flight per thread.
 constexpr int kCheckItems = 4;
 
-template <int D>
-__global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundParams P) {
+template <int D, bool STRIDED = false>
+__device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
   constexpr int ITEMS = D > 0 ? kCheckItems : 1;
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
@@ -743,10 +897,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
   // sorted, degree-renumbered instance the candidate density grows steadily along the id space (hub
   // regions hold almost none), and consecutive regions per claim left the last claims with all the work.
   const uint32_t stride = (P.nseg + P.check_claim - 1u) / P.check_claim;
-  for (uint32_t ticket = grid_warp();; ticket = claim_region(&c->ticket_c, lane, true)) {
+  for (uint32_t ticket = grid_warp();;
+       ticket = STRIDED ? ticket + gridDim.x * kWarpsPerBlock : claim_region(&c->ticket_c, lane, true)) {
     if (ticket >= stride) break;
     // end[j] = candidates in the first j+1 regions of the claim (inclusive prefix), the same in every lane
-    uint32_t mine = (lane < P.check_claim && ticket + lane * stride < P.nseg) ? list_cnt[ticket + lane * stride] : 0u;
+    uint32_t mine = (lane < P.check_claim && ticket + lane * stride < P.nseg) ? __ldcg(list_cnt + ticket + lane * stride) : 0u;
 #pragma unroll
     for (int o = 1; o < static_cast<int>(kCoarseClaim); o <<= 1) {
       const uint32_t t = __shfl_up_sync(0xffffffffu, mine, o);
@@ -770,7 +925,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
             j = q + 1;
             begin = end[q];
           }
-        e[k] = valid[k] ? list[static_cast<size_t>(ticket + j * stride) * P.seg_cap + (idx - begin)] : 0u;
+        e[k] = valid[k] ? __ldcg(list + static_cast<size_t>(ticket + j * stride) * P.seg_cap + (idx - begin)) : 0u;
       }
       if constexpr (D > 0) {
         PinVec<D> pv[ITEMS];
@@ -849,6 +1004,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
     const uint32_t mp = warp_sum(local_mpins);  // a warp matches far fewer than 2^32 pins per launch
     if (lane == 0 && mp) atomicAdd(&c->pins_matched, static_cast<unsigned long long>(mp));
   }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundParams P) {
+  check_commit_small_body<D>(P);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -983,8 +1143,7 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
 
 // One thread.  Round bookkeeping between check/commit of round r and the filter of round r+1;
 // sets the WHILE condition of the enclosing CUDA graph when there is one.
-__global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle, int in_graph,
-                          uint32_t active_elsewhere) {
+__device__ __forceinline__ uint32_t advance_round(const RoundParams& P, uint32_t active_elsewhere) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round, par = c->parity;
   const uint32_t active = c->active_small + c->count1[par ^ 1];
@@ -1012,7 +1171,205 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
     if (r % P.ks.tag_period == 0) status = ST_EPOCH;
   }
   c->status = status;
+  return status;
+}
+
+__global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle, int in_graph,
+                          uint32_t active_elsewhere) {
+  const uint32_t status = advance_round(P, active_elsewhere);
   if (in_graph) cudaGraphSetConditional(handle, status == ST_RUNNING ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------------------------
+// All rounds of a small uniform instance in ONE cooperative launch.  When the whole instance sits
+// in L2 a round is a handful of dependent memory round trips, and three kernel launches per round
+// (sweep, check, advance: ~85 us per round inside the CUDA graph on config 1) cost several times
+// the work itself.  Here the resident grid runs sweep -> grid barrier -> check -> grid barrier ->
+// advance (one thread) -> grid barrier, round after round, until the status leaves ST_RUNNING (done,
+// round cap, tie, tag wrap: the host handles those exactly as after a graph launch).  The phases are
+// the bodies of the stand-alone kernels, so the results are the same by construction; the lists and
+// per-vertex words written in one phase are read in the next after the barrier's fence (the barrier of
+// cooperative groups ends with MEMBAR.GPU + CCTL.IVALL in every CTA, so ld.ca lines of the hot windows do
+// not survive a phase; the lists use ld.cg).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void grid_zero(void* p, size_t bytes) {  // bytes: a multiple of 4, p 16-byte aligned
+  const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x, nth = static_cast<size_t>(gridDim.x) * blockDim.x;
+  uint4* q = static_cast<uint4*>(p);
+  const size_t vec = (reinterpret_cast<uintptr_t>(p) & 15u) ? 0 : bytes >> 4;
+  for (size_t i = tid; i < vec; i += nth) q[i] = make_uint4(0u, 0u, 0u, 0u);
+  uint32_t* t = static_cast<uint32_t*>(p) + (vec << 2);
+  const size_t rest = (bytes >> 2) - (vec << 2);
+  for (size_t i = tid; i < rest; i += nth) t[i] = 0u;
+}
+
+#ifndef HLM_FUSED_ITEMS
+#define HLM_FUSED_ITEMS(D) ((D) == 2 ? 4 : ((D) == 4 ? 2 : 1))
+#endif
+// PIPE: the software-pipelined sweep (four batches in flight per warp, more registers) instead of the plain one
+template <int D, bool PIPE>
+__global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_fused(const RoundParams P, const FusedExtra X) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ uint32_t s_warp[kWarpsPerBlock];
+  __shared__ unsigned long long s_sum[kWarpsPerBlock];
+#ifdef HLM_FUSED_TRACE
+  uint32_t tr_n = 0;
+#define FUSED_MARK()                                                                     \
+  do {                                                                                   \
+    if (X.sum && blockIdx.x == 0 && threadIdx.x == 0 && tr_n < 64u) {                    \
+      unsigned long long t;                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                              \
+      X.sum->trace[tr_n++] = t;                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define FUSED_MARK() do {} while (0)
+#endif
+  FUSED_MARK();
+  if (X.init) {
+    grid_zero(P.vkey, static_cast<size_t>(P.n) * 8);
+    grid_zero(P.vtop, static_cast<size_t>(P.n) * 4);
+    grid_zero(P.dead, ((static_cast<size_t>(P.n) + 31) / 32) * 4);
+    grid_zero(P.mbits, static_cast<size_t>(X.mbits_words) * 4);
+    grid_zero(P.matched_cnt, static_cast<size_t>(X.rounds_cap) * 4);
+    grid_zero(P.deact_cnt, static_cast<size_t>(X.rounds_cap) * 4);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctrl = X.c0;
+    grid.sync();
+    FUSED_MARK();
+  }
+  uint32_t status;
+  for (;;) {
+    if constexpr (PIPE) sweep_uniform_body<D, true, false, true>(P, nullptr);
+    else sweep_uniform_ilp_body<D, HLM_FUSED_ITEMS(D)>(P);
+    FUSED_MARK();
+    grid.sync();
+    FUSED_MARK();
+    check_commit_small_body<D, true>(P);
+    FUSED_MARK();
+    // the block that finishes the check last does the round bookkeeping: two grid barriers per round
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&P.ctrl->blocks_done, 1u) == gridDim.x - 1u) {
+        __threadfence();
+        P.ctrl->blocks_done = 0u;
+        advance_round(P, 0u);
+      }
+    }
+    grid.sync();
+    FUSED_MARK();
+    status = *reinterpret_cast<volatile uint32_t*>(&P.ctrl->status);
+    if (status != ST_RUNNING) break;
+  }
+  if (!X.sum) return;
+  const Ctrl* c = P.ctrl;
+  const uint32_t rounds = c->rounds_done;
+  const bool finished = (status == ST_DONE || status == ST_ROUND_LIMIT) && rounds <= kFusedRounds;
+  if (!finished) {  // tie / tag wrap: the host takes over and assembles the result the usual way
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      X.sum->ctrl = *c;
+      X.sum->assembled = 0u;
+    }
+    return;
+  }
+  // ---- finish_matching (local_max_seq.hpp:74-83): matched ids in ascending order, straight into the
+  // caller's page-locked arrays.  Every block owns a contiguous range of bitmap words, every thread a
+  // contiguous piece of it: count, prefix over the blocks, write.
+  const uint32_t per_block = (X.mbits_words + gridDim.x - 1u) / gridDim.x;
+  const uint32_t per_thread = (per_block + kBlock - 1u) / kBlock;
+  const uint32_t b1 = min(X.mbits_words, (blockIdx.x + 1u) * per_block);
+  const uint32_t w0 = min(b1, blockIdx.x * per_block + threadIdx.x * per_thread);
+  const uint32_t w1 = min(b1, w0 + per_thread);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t cnt = 0;
+  unsigned long long wsum = 0;
+  for (uint32_t w = w0; w < w1; ++w) {
+    uint32_t b = __ldcg(P.mbits + w);
+    cnt += __popc(b);
+    if (X.base_int)
+      while (b) {
+        const uint32_t bit = __ffs(b) - 1u;
+        b &= b - 1u;
+        wsum += static_cast<unsigned long long>(__ldg(X.base_int + (w * 32u + bit)));
+      }
+  }
+  uint32_t incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += t;
+  }
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if (lane == 31) s_warp[warp] = incl;
+  if (lane == 0) s_sum[warp] = wsum;
+  __syncthreads();
+  uint32_t before_warp = 0, block_total = 0;
+#pragma unroll
+  for (int w = 0; w < kWarpsPerBlock; ++w) {
+    if (w < static_cast<int>(warp)) before_warp += s_warp[w];
+    block_total += s_warp[w];
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kWarpsPerBlock; ++w) t += s_sum[w];
+    X.block_cnt[blockIdx.x] = block_total;
+    X.block_isum[blockIdx.x] = t;
+  }
+  grid.sync();
+  uint32_t mine = 0, every = 0;
+  for (uint32_t i = threadIdx.x; i < gridDim.x; i += kBlock) {
+    const uint32_t v = __ldcg(X.block_cnt + i);
+    every += v;
+    if (i < blockIdx.x) mine += v;
+  }
+  const uint32_t before_block = block_sum(mine, s_warp);
+  const uint32_t total = block_sum(every, s_warp);
+  const bool fits = total <= X.out_cap;  // (always: out_cap is an upper bound of any matching's size)
+  uint32_t o = before_block + before_warp + incl - cnt;
+  if (fits) {
+    for (uint32_t w = w0; w < w1; ++w) {
+      uint32_t b = __ldcg(P.mbits + w);
+      while (b) {
+        const uint32_t bit = __ffs(b) - 1u;
+        b &= b - 1u;
+        const uint32_t e = w * 32u + bit;
+        X.dev_ids[o] = e + P.id_base;
+        if (X.out_round) X.dev_round[o] = __ldcg(P.mround + e);
+        ++o;
+      }
+    }
+    // device staging -> the caller's page-locked arrays, 16 bytes per thread and store: scattered 4-byte
+    // stores across the bus cost a transaction each (config 1: 0.25 ms for 144 K ids)
+    grid.sync();
+    const uint32_t tid = blockIdx.x * kBlock + threadIdx.x, nth = gridDim.x * kBlock;
+    const uint4* src = reinterpret_cast<const uint4*>(X.dev_ids);
+    uint4* dst = reinterpret_cast<uint4*>(X.out_ids);
+    for (uint32_t i = tid; i < (total + 3u) / 4u; i += nth) dst[i] = __ldcg(src + i);
+    if (X.out_round) {
+      src = reinterpret_cast<const uint4*>(X.dev_round);
+      dst = reinterpret_cast<uint4*>(X.out_round);
+      for (uint32_t i = tid; i < (total + 7u) / 8u; i += nth) dst[i] = __ldcg(src + i);
+    }
+  }
+  FUSED_MARK();
+  if (blockIdx.x == gridDim.x - 1u) {  // the last block also writes the summary
+    unsigned long long t = 0;
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += kBlock) t += __ldcg(X.block_isum + i);
+    for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
+    __syncthreads();
+    if (lane == 0) s_sum[warp] = t;
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r <= rounds + 1u && r < kFusedRounds + 2u; r += kBlock) {
+      X.sum->matched[r] = __ldcg(P.matched_cnt + r);
+      X.sum->dropped[r] = __ldcg(P.deact_cnt + r);
+    }
+    if (threadIdx.x == 0) {
+      unsigned long long all = 0;
+      for (int w = 0; w < kWarpsPerBlock; ++w) all += s_sum[w];
+      X.sum->ctrl = *c;
+      X.sum->total = total;
+      X.sum->isum = all;
+      X.sum->assembled = fits ? 1u : 0u;
+    }
+  }
 }
 
 // Round tags wrapped: forget every running maximum but keep the dead marks.

@@ -53,10 +53,42 @@ struct Ctrl {
   uint32_t max_rounds;
   uint32_t rounds_done;
   uint32_t active_prev;  // class-0 edges in the list the next sweep reads (0 before round 2)
+  uint32_t blocks_done;  // fused kernel: CTAs that finished this round's check
+  uint32_t pad0;
   unsigned long long edges_swept;  // sum over rounds of the active-list lengths (sum of m_r)
   unsigned long long pins_swept;   // sum over rounds of the pins of the active edges (sum of kappa_r)
   unsigned long long pins_round;   // ragged instances: pins of the edges kept by this round's sweeps
   unsigned long long pins_matched; // ragged instances: pins of all matched edges so far
+};
+
+// One-launch matching of a small instance (k_rounds_fused): what the kernel leaves in page-locked host
+// memory for the caller -- nothing else crosses the bus, and nothing is read back before the one final sync.
+constexpr uint32_t kFusedRounds = 254;
+struct FusedSummary {
+  Ctrl ctrl;                 // the final control block
+  unsigned long long total;  // matched edges
+  unsigned long long isum;   // sum of their (integer) base weights, when asked for
+  uint32_t assembled;        // 1: ids / rounds / per-round counts below are in place
+  uint32_t pad;
+  uint32_t matched[kFusedRounds + 2];  // [r] edges matched in round r
+  uint32_t dropped[kFusedRounds + 2];  // [r] edges dropped from the list after round r
+  unsigned long long trace[64];        // -DHLM_FUSED_TRACE: globaltimer of block 0 at every phase boundary
+};
+
+struct FusedExtra {
+  Ctrl c0;                 // init: the control block of a fresh run
+  uint32_t init;           // zero the per-call state (filter words, keys, bitmaps, counters) first
+  uint32_t rounds_cap;     // entries of matched_cnt / deact_cnt
+  uint32_t mbits_words;
+  uint32_t out_cap;        // entries of out_ids / out_round
+  uint32_t* block_cnt;     // [grid] scratch of the assembly phase
+  unsigned long long* block_isum;  // [grid]
+  uint32_t* dev_ids;       // [out_cap + 4] device staging of the result (the bus wants full-line writes)
+  uint16_t* dev_round;     // [out_cap + 8]
+  uint32_t* out_ids;       // page-locked host memory, same sizes (or null together with sum)
+  uint16_t* out_round;     // may be null
+  const double* base_int;  // non-null: integer base weights (caller-id indexed), summed on the device
+  FusedSummary* sum;       // page-locked host memory; null: rounds only, no assembly
 };
 
 struct EdgeCsr {
