@@ -1824,8 +1824,11 @@ int assemble_result(Graph* g, uint32_t rounds, const hlm_b200_config* cfg, int v
 // first pin, which only the CRCW sweeps gain from)
 bool crcw_is_faster(const Graph* g) {
   const uint64_t vtop_bytes = static_cast<uint64_t>(g->n) * 4, l2 = static_cast<uint64_t>(g->l2_bytes);
+  // (8-uniform below ~4 M pins: the one-launch kernel of small instances, 0.27 against 0.34 ms at 2 M pins;
+  // at 8 M pins the vertex-owned kernels are ahead again, 0.45 against 0.57 ms)
   return g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
-         (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4);
+         (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4) ||
+         (g->uniform_d == 8 && !g->num_large && g->kappa <= (1ull << 22));
 }
 
 int run_match(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, hlm_b200_result* out) {

@@ -5,10 +5,9 @@ sys.path.insert(0, ".")
 import numpy as np
 import paper_2602_22976_b200 as hb
 
-def run(dg, ws, fused, ctas=None):
+def run(dg, ws, fused, variant="crcw"):
     os.environ["HLM_B200_FUSED_MAX_PINS"] = str(1 << 40) if fused else "0"
-    if ctas: os.environ["HLM_B200_FUSED_CTAS"] = str(ctas)
-    cfg = hb.ParallelConfig(variant="crcw", loop_mode="graph")
+    cfg = hb.ParallelConfig(variant=variant, loop_mode="graph")
     for _ in range(5):
         r = dg.match(ws, cfg)
     ds = []
@@ -18,7 +17,7 @@ def run(dg, ws, fused, ctas=None):
     return r, min(ds), sorted(ds)[15]
 
 ws = hb.WeightStream()
-for (n, m, d) in ((1000, 1000, 4), (1_000_000, 1_000_000, 4), (100_000, 300_000, 2), (250_000, 250_000, 8), (2_000_000, 2_000_000, 4), (2_000_000, 8_000_000, 2)):
+for (n, m, d) in ((1000, 1000, 4), (1_000_000, 1_000_000, 4), (100_000, 300_000, 2), (250_000, 250_000, 8), (2_000_000, 2_000_000, 4), (2_000_000, 8_000_000, 2), (500_000, 1_000_000, 8), (4_000_000, 4_000_000, 2)):
     host = hb.generate_random(n, m, d, d, 1)
     dg = hb.DeviceHypergraph.upload(host)
     b, tb, mb = run(dg, ws, True)
@@ -31,5 +30,8 @@ for (n, m, d) in ((1000, 1000, 4), (1_000_000, 1_000_000, 4), (100_000, 300_000,
             and a.report.matched_per_round_count == b.report.matched_per_round_count
             and a.report.deactivated_per_round == b.report.deactivated_per_round
             and a.matching.total_weight == b.matching.total_weight)
+    c, tc, mc = run(dg, ws, True, "crew")
+    d_, td, md = run(dg, ws, True, "auto")
+    print(f"     vertex-owned {tc:.3f} ms, auto {td:.3f} ms (engine {d_.report.engine})")
     print(f"n={n} m={m} d={d}: same={same} rounds {a.report.rounds}/{b.report.rounds} graph {ta:.3f} (med {ma:.3f}) fused {tb:.3f} (med {mb:.3f}) ms launches {a.report.kernel_launches}/{b.report.kernel_launches}", flush=True)
     dg.release()

@@ -166,7 +166,8 @@ def test_vertex_owned_run_finished_by_the_crcw_kernels(hb, port, monkeypatch):
     monkeypatch.setenv("HLM_B200_CREW_TAIL", "100000")  # percent of n alive pins: always true from round 2 on
     cases = [
         ("netlist", po.SYN_NETLIST, dict(n=60_000, m=120_000), True),
-        ("uniform", po.SYN_UNIFORM, dict(n=40_000, m=90_000, d=8), False),
+        # (above 4 M pins: smaller 8-uniform instances belong to the CRCW engine and are loaded in its edge order)
+        ("uniform", po.SYN_UNIFORM, dict(n=280_000, m=560_000, d=8), False),
         ("powerlaw", po.SYN_POWERLAW, dict(n=50_000, m=100_000), False),
     ]
     streams = [po.Stream(seed=4), po.Stream(seed=4, noise_high=0.0), po.Stream(seed=8, kind=po.GEN_PARK_MILLER, noise_high=2.0 ** -50),
