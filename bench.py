@@ -392,7 +392,9 @@ def measure(hb, torch, np, dg, wl, steps, warmup, tstream, hbm_gbs):
                               "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_gbs}}
     out = dict(kappa=kappa, m=m, n=n, ms_per_step=ms_per_step, total_ms=total_ms, value=kappa * steps / (total_ms * 1e-3),
                launches=int(launches), dev_ms=float(np.mean(dev_ms)), res=res, roofline=roofline,
-               engine=res.report.engine + " (one CUDA-graph launch per matching)")
+               engine=res.report.engine + (" (ONE cooperative kernel launch per matching: k_rounds_fused = state reset, "
+                                           "all rounds, result assembly)" if res.report.kernel_launches == 1
+                                           else " (one CUDA-graph launch per matching)"))
     return out
 
 

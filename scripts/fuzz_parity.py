@@ -26,7 +26,9 @@ def same(got, want):
     return (np.array_equal(got.matching.matched_edges, want.matched_edges) and got.report.rounds == want.rounds
             and got.report.matched_per_round_count == want.per_round_matched
             and got.report.deactivated_per_round == want.per_round_deactivated
-            and got.matching.total_weight == want.total_weight)
+            and got.matching.total_weight == want.total_weight
+            and (got.report.matched_round is None
+                 or np.array_equal(got.report.matched_round.astype(np.uint32), want.matched_round)))
 
 
 def rand_stream():
@@ -45,6 +47,8 @@ def rand_graph(medium):
     lo = int(rng.integers(1, 4))
     hi = min(n, lo + int(rng.choice([0, 1, 3, 8, 40])))
     lo = min(lo, hi)
+    if rng.random() < 0.3:  # uniform 2 / 4 / 8: the one-launch kernel of small instances (k_rounds_fused)
+        lo = hi = min(n, int(rng.choice([2, 4, 8])))
     g = port.generate_random(n, m, lo, hi, int(rng.integers(0, 2 ** 31)))
     w = int(rng.integers(0, 4))
     if w == 1:
@@ -76,7 +80,12 @@ while time.time() < t_end and not bad:
     dg = hb.DeviceHypergraph.upload(hg)
     os.environ.pop("HLM_B200_AUTO", None)
     os.environ.pop("HLM_B200_CREW_TAIL", None)
-    check("crcw graph", dg.match(hs, hb.ParallelConfig(variant="crcw", loop_mode="graph")), want, what)
+    r = dg.match(hs, hb.ParallelConfig(variant="crcw", loop_mode="graph"))
+    check("crcw graph", r, want, what)
+    if r.report.kernel_launches == 1:
+        check("crcw graph, one launch", r, want, what)
+        check("crcw graph, one launch, no round record",
+              dg.match(hs, hb.ParallelConfig(variant="crcw", loop_mode="graph", want_round_of=False)), want, what)
     check("crcw host", dg.match(hs, hb.ParallelConfig(variant="crcw", loop_mode="host")), want, what)
     check("crcw exact ties", dg.match(hs, hb.ParallelConfig(variant="crcw", tie_mode="exact")), want, what)
     check("crew graph", dg.match(hs, hb.ParallelConfig(variant="crew")), want, what)

@@ -3,7 +3,7 @@
 out=gpurun_out/sanitizer_r02.txt
 : > $out
 run() { echo "== $*" >> $out; timeout 900 "$@" 2>&1 | grep -E "passed|failed|ERROR SUMMARY|RACECHECK SUMMARY|same|DIFFERENT|ok=|Error|error" | tail -12 >> $out; }
-K="test_gpu_multi or test_gpu_variants or edge_case or loader or test_crew"
+K="test_gpu_multi or test_gpu_variants or test_gpu_fused or edge_case or loader or test_crew"
 run compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -k "$K"
 run compute-sanitizer --tool initcheck python -m pytest tests -m gpu -q -k "$K"
 HLM_B200_CREW_HOST_LOOP=1 FIRST_VARIANT=crew run compute-sanitizer --tool racecheck python scripts/crew_small.py
