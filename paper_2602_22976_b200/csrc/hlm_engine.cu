@@ -1261,7 +1261,7 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
 // CUDA graph: below ~8 M pins the three launches per round cost more than the round.  The limit is the pin
 // count of the whole instance (HLM_B200_FUSED_MAX_PINS overrides it; 0 disables the fused loop).
 static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
-  if (L.exact || g->num_large) return false;
+  if (L.exact || g->num_large || g->fused_off) return false;
   if (g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
   uint64_t limit = 1ull << 23;
   if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) limit = std::strtoull(env, nullptr, 10);
@@ -1313,8 +1313,32 @@ static int launch_fused_rounds(Graph* g, Launcher& L, const FusedExtra* extra) {
   const void* fn = fused_kernel(g);
   ST_CHECK(fused_grid_size(g, fn));
   void* args[] = {&P, &X};
-  CU_CHECK(cudaLaunchCooperativeKernel(fn, dim3(g->fused_grid), dim3(kBlock), args, 0, g->stream));
+  const cudaError_t e = std::getenv("HLM_B200_FUSED_REFUSE")  // test hook: behave as if the launch had been refused
+                            ? cudaErrorCooperativeLaunchTooLarge
+                            : cudaLaunchCooperativeKernel(fn, dim3(g->fused_grid), dim3(kBlock), args, 0, g->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported || e == cudaErrorLaunchOutOfResources) {
+    // fewer SMs than the device reports (MPS share, green context): this instance uses the graph loop instead
+    cudaGetLastError();
+    g->fused_off = true;
+    return HLM_B200_OK;
+  }
+  CU_CHECK(e);
   ++L.launches;
+  return HLM_B200_OK;
+}
+
+// the per-call state of a CRCW run (what k_rounds_fused does in its first phase when it runs the whole call)
+static int reset_match_state(Graph* g, const Ctrl& c0) {
+  Workspace& w = g->ws;
+  cudaStream_t s = g->stream;
+  CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+  CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
+  CU_CHECK(cudaMemsetAsync(w.vtop, 0, static_cast<size_t>(g->n) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+  CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
+  if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
   return HLM_B200_OK;
 }
 
@@ -1407,6 +1431,11 @@ static int crcw_run(Graph* g, Launcher& L, uint32_t max_rounds, bool use_graph, 
       bool have_ctrl = false;
       if (use_graph && fused_rounds_ok(g, L)) {
         ST_CHECK(launch_fused_rounds(g, L, S.fused));
+        if (g->fused_off) {  // refused: nothing ran; the state reset the kernel would have done, then the graph loop
+          if (S.fused && S.fused->init) ST_CHECK(reset_match_state(g, S.fused->c0));
+          S.fused = nullptr;
+          continue;
+        }
         ++graph_launches;
         if (S.fused) {
           S.fused->init = 0u;  // a relaunch (after a tie or a tag wrap) continues the run
@@ -1548,16 +1577,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   bool fused_all = false;
   std::memset(&fx, 0, sizeof(fx));
   if (use_graph && g->m && !greedy && fused_rounds_ok(g, L)) ST_CHECK(fused_prepare(g, cfg, c0, &fx, &pre, &fused_all));
-  if (!fused_all) {
-    CU_CHECK(cudaMemcpyAsync(w.ctrl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
-    CU_CHECK(cudaMemsetAsync(w.vkey, 0, static_cast<size_t>(g->n) * 8, s));
-    CU_CHECK(cudaMemsetAsync(w.vtop, 0, static_cast<size_t>(g->n) * 4, s));
-    CU_CHECK(cudaMemsetAsync(w.dead, 0, ((static_cast<size_t>(g->n) + 31) / 32) * 4, s));
-    CU_CHECK(cudaMemsetAsync(w.mbits, 0, static_cast<size_t>(w.mbits_words) * 4, s));
-    CU_CHECK(cudaMemsetAsync(w.matched_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
-    CU_CHECK(cudaMemsetAsync(w.deact_cnt, 0, static_cast<size_t>(w.rounds_cap) * 4, s));
-    if (g->num_large) CU_CHECK(cudaMemsetAsync(w.large_state, LARGE_ACTIVE, g->num_large, s));
-  }
+  if (!fused_all) ST_CHECK(reset_match_state(g, c0));
 
   Ctrl c = c0;
   CrcwRunStats S;

@@ -120,6 +120,7 @@ struct Graph {
   uint64_t device_bytes = 0;
   uint64_t h2d_bytes = 0;
   int round_grid = 0, sweep_grid = 0, check_grid = 0, large_grid = 0, fused_grid = 0;
+  bool fused_off = false;  // a cooperative launch was refused (SM-limited context): the graph loop from then on
   Workspace ws;
   CrewState* crew = nullptr;
   EdgeCsr csr() const;

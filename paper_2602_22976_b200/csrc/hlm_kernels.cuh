@@ -1342,11 +1342,13 @@ __global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_
     const uint32_t tid = blockIdx.x * kBlock + threadIdx.x, nth = gridDim.x * kBlock;
     const uint4* src = reinterpret_cast<const uint4*>(X.dev_ids);
     uint4* dst = reinterpret_cast<uint4*>(X.out_ids);
-    for (uint32_t i = tid; i < (total + 3u) / 4u; i += nth) dst[i] = __ldcg(src + i);
+    for (uint32_t i = tid; i < total / 4u; i += nth) dst[i] = __ldcg(src + i);
+    if (tid < (total & 3u)) X.out_ids[(total & ~3u) + tid] = __ldcg(X.dev_ids + (total & ~3u) + tid);  // tail, by entry
     if (X.out_round) {
       src = reinterpret_cast<const uint4*>(X.dev_round);
       dst = reinterpret_cast<uint4*>(X.out_round);
-      for (uint32_t i = tid; i < (total + 7u) / 8u; i += nth) dst[i] = __ldcg(src + i);
+      for (uint32_t i = tid; i < total / 8u; i += nth) dst[i] = __ldcg(src + i);
+      if (tid < (total & 7u)) X.out_round[(total & ~7u) + tid] = __ldcg(X.dev_round + (total & ~7u) + tid);
     }
   }
   FUSED_MARK();

@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, ".")
 import paper_2602_22976_b200 as hb
 ws = hb.WeightStream()
-for (n, m, d) in ((1000, 1000, 4), (1_000_000, 1_000_000, 4)):
+for (n, m, d) in (((1_000_000, 1_000_000, 4),) if len(sys.argv) > 1 else ((1000, 1000, 4), (1_000_000, 1_000_000, 4))):
     host = hb.generate_random(n, m, d, d, 1)
     dg = hb.DeviceHypergraph.upload(host)
     cfg = hb.ParallelConfig(variant="crcw", loop_mode="graph")

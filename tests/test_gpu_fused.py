@@ -90,3 +90,21 @@ def test_one_launch_kernel_switched_off_gives_the_same(hb, port, monkeypatch):
         assert other.report.deactivated_per_round == fused.report.deactivated_per_round
         assert other.matching.total_weight == fused.matching.total_weight
     dg.release()
+
+
+def test_refused_cooperative_launch_falls_back_to_the_graph_loop(hb, port, monkeypatch):
+    """An SM-limited context (MPS share, green context) can refuse the cooperative launch: the instance then
+    runs on the CUDA-graph loop, in that call and in every later one, with the same result."""
+    g = port.syn_generate(po.SYN_UNIFORM, n=20_000, m=40_000, d=4, seed=9, int_weights=True)
+    s = po.Stream(seed=6)
+    want = port.local_max(g, s)
+    dg = hb.DeviceHypergraph.upload(to_hb_graph(g))
+    monkeypatch.setenv("HLM_B200_FUSED_REFUSE", "1")
+    got = dg.match(to_hb_stream(s), hb.ParallelConfig(variant="crcw"))
+    assert_same_result(got, want, "refused launch")
+    assert got.report.kernel_launches > 1
+    monkeypatch.delenv("HLM_B200_FUSED_REFUSE")
+    again = dg.match(to_hb_stream(s), hb.ParallelConfig(variant="crcw"))  # stays on the graph loop
+    assert_same_result(again, want, "after a refused launch")
+    assert again.report.kernel_launches > 1
+    dg.release()
