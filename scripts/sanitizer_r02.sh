@@ -9,5 +9,9 @@ run compute-sanitizer --tool initcheck python -m pytest tests -m gpu -q -k "$K"
 HLM_B200_CREW_HOST_LOOP=1 FIRST_VARIANT=crew run compute-sanitizer --tool racecheck python scripts/crew_small.py
 FIRST_VARIANT=crew run compute-sanitizer --tool memcheck python scripts/crew_small.py
 run compute-sanitizer --tool memcheck python scripts/shard_check.py uniform 20000 30000 4 1,3
-run compute-sanitizer --tool racecheck python scripts/shard_check.py powerlaw 20000 40000 0 2
+# racecheck follows neither conditional graph nodes nor NCCL's kernels: host-driven loops, co-located exchange
+HLM_B200_CREW_HOST_LOOP=1 run compute-sanitizer --tool racecheck python scripts/shard_check.py powerlaw 20000 40000 0 2 nonccl
+# the one-launch kernel of small instances (cooperative grid, shared-memory scans, grid barriers)
+run compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_fused.py -m gpu -q
+run compute-sanitizer --tool synccheck python -m pytest tests/test_gpu_fused.py -m gpu -q
 cat $out

@@ -11,7 +11,8 @@ for ws in (hb.WeightStream(), hb.WeightStream(noise_high=0.0)):
     print("single crew", ref.report.rounds, len(ref.matching.matched_edges), ref.report.matched_per_round_count, ref.report.deactivated_per_round)
     for w in worlds:
         shards = mg.generate_shards(fam, w, **spec)
-        for comm in (None, mg.Communicator.create(None, 0, 1, 0)):
+        # "nonccl" as 6th argument: co-located exchange only (racecheck cannot follow NCCL's kernels)
+        for comm in ((None,) if len(sys.argv) > 6 and sys.argv[6] == "nonccl" else (None, mg.Communicator.create(None, 0, 1, 0))):
             for tie in ("auto", "exact"):
                 t0 = time.time()
                 res, rep = mg.match_sharded(shards, ws, hb.ParallelConfig(tie_mode=tie), comm)
