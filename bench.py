@@ -402,7 +402,7 @@ def config_entry(name, wl, r):
     rep = r["res"].report
     return {"name": name, "workload": wl["desc"], "pins": r["kappa"], "edges": r["m"], "vertices": r["n"],
             "variant": "auto", "engine": r["engine"], "rounds": rep.rounds, "matched": int(len(r["res"].matching.matched_edges)),
-            "ms": r["ms_per_step"], "pins_per_s": r["value"], "whole_job_frac": r["roofline"]["whole_job"]["frac"],
+            "ms": r["ms_per_step"], "device_ms": r["dev_ms"], "pins_per_s": r["value"], "whole_job_frac": r["roofline"]["whole_job"]["frac"],
             "dominant_kernel": r["roofline"]["kernel"].split(":")[0], "dominant_frac": r["roofline"]["frac"],
             "dominant_round1_frac": r["roofline"]["round1_frac"], "dominant_share_of_step": r["roofline"]["share_of_step"],
             "algorithmic_bytes": r["roofline"]["whole_job"]["algorithmic_bytes"]}
@@ -549,7 +549,10 @@ def main():
             try:
                 g2 = make_instance(hb, WORKLOADS[name], local_rank)
                 r2 = measure(hb, torch, np, g2, WORKLOADS[name], 5, 3, tstream, hbm_gbs)
+                if r2["ms_per_step"] < 2.0:  # a sub-millisecond matching: five calls time the first-call effects
+                    r2 = measure(hb, torch, np, g2, WORKLOADS[name], 50, 5, tstream, hbm_gbs)
                 entries[name] = config_entry(name, WORKLOADS[name], r2)
+                entries[name]["steps"] = 50 if r2["ms_per_step"] < 2.0 else 5
                 g2.release()
                 del r2
             except Exception as exc:  # one config must not cost the headline line

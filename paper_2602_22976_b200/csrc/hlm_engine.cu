@@ -1320,6 +1320,8 @@ static int launch_fused_rounds(Graph* g, Launcher& L, const FusedExtra* extra) {
     // fewer SMs than the device reports (MPS share, green context): this instance uses the graph loop instead
     cudaGetLastError();
     g->fused_off = true;
+    if (std::getenv("HLM_B200_TRACE"))
+      std::fprintf(stderr, "[hlm_b200] cooperative launch of %d CTAs refused (%s): graph loop\n", g->fused_grid, cudaGetErrorString(e));
     return HLM_B200_OK;
   }
   CU_CHECK(e);
