@@ -436,6 +436,12 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the matching path has no CPU fallback")
+    # HLM_BENCH_ONE_GPU=1: dry run of the N-rank path on a box with one device (tests/test_gpu_multi.py): every
+    # rank uses device 0, gloo carries the communicator id, and HLM_B200_NCCL_LIB must name a transport that
+    # accepts several ranks per device (NCCL does not).  Not a measurement.
+    one_gpu = os.environ.get("HLM_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     # HLM_BENCH_FORCE_MG=1 runs the edge-partitioned (multi-GPU) driver even with one rank: the only
     # way to exercise that code path on a single-GPU box
@@ -457,7 +463,10 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29511")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist_mod.init_process_group("gloo")
+        else:
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2602_22976_b200 import multi_gpu
 
         multi_gpu.bench_main(args, wl, rank, world, local_rank, dist_mod,

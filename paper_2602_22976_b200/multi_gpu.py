@@ -173,14 +173,15 @@ def generate_shards(family: str, world: int, device: int = 0, **spec) -> List[De
     return out
 
 
-def upload_shards(h, world: int, device: int = 0) -> List[DeviceHypergraph]:
-    """The edge rows of a host Hypergraph cut into `world` blocks, each loaded as a shard on `device`."""
+def upload_shards(h, world: int, device: int = 0, only_rank: Optional[int] = None) -> List[DeviceHypergraph]:
+    """The edge rows of a host Hypergraph cut into `world` blocks, each loaded as a shard on `device`
+    (only_rank: just that rank's block -- one process per rank)."""
     lib = _lib.load_library()
     out = []
     eo = np.ascontiguousarray(h.edge_offsets, dtype=np.uint64)
     pins = np.ascontiguousarray(h.edge_members, dtype=np.uint32)
     base = np.ascontiguousarray(h.base_weights, dtype=np.float64)
-    for r in range(world):
+    for r in (range(world) if only_rank is None else [only_rank]):
         b, k = shard_bounds(h.num_edges, world, r)
         if not k:
             continue
@@ -230,7 +231,7 @@ def bench_main(args, wl, rank, world, local_rank, dist, extras=None):
         launches += rep["kernel_launches"]
     ev1.record(tstream)
     torch.cuda.synchronize()
-    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
     clocks = sampler.stop() if sampler else None
