@@ -459,12 +459,41 @@ __device__ __forceinline__ void sweep_uniform_simple_body(const RoundParams& P) 
   if (tie) c->tie_flag = 1u;
 }
 
+// MERGED (fused kernel, d = 2 / 4): the filter word of a vertex is the high half of its 64-bit key in place --
+// no second array and no second atomic per deposit.  An instance this small keeps vkey (8 B per vertex) in L2,
+// which is what the separate 4-byte array exists for elsewhere; round 1 of config 1 is bound by the L2's
+// atomic rate (8 M atomicMax -> 4 M: 50 -> 27 us).  A covered vertex holds all-ones in both halves.
+__device__ __forceinline__ const uint32_t* top_half(const RoundParams& P, uint32_t v) {
+  return reinterpret_cast<const uint32_t*>(P.vkey + v) + 1;  // little-endian: the high word
+}
+template <bool MERGED>
+__device__ __forceinline__ uint32_t ld_top_x(const RoundParams& P, uint32_t v) {
+  if constexpr (!MERGED) return ld_top(P, v);
+  else return v < P.hot_vtop ? __ldca(top_half(P, v)) : __ldcg(top_half(P, v));
+}
+template <bool MERGED>
+__device__ __forceinline__ bool deposit_key_x(const RoundParams& P, uint32_t v, unsigned long long key, uint32_t cur) {
+  if constexpr (!MERGED) return deposit_key(P, v, key, cur);
+  else {
+    if (cur > static_cast<uint32_t>(key >> 32)) return false;
+    return atomicMax(P.vkey + v, key) == key;
+  }
+}
+template <bool MERGED>
+__device__ __forceinline__ void mark_dead_x(const RoundParams& P, uint32_t v) {
+  if constexpr (!MERGED) mark_dead(P, v);
+  else {
+    P.vkey[v] = ~0ull;
+    atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+  }
+}
+
 // The sweep of the fused small-instance kernel: the same decisions as the plain sweep, ITEMS batches of a
 // region per step with the loads of all of them issued together.  A small instance is latency-bound -- the
 // resident warps each walk a few batches one dependent L2 round trip after the other (config 1: 6.6 batches
 // per warp, ~5 trips each) -- so the trips of ITEMS batches overlap.  Regions by warp index (no tickets);
 // deactivation always on the dead bitmap (identical to the kTopDead test: mark_dead sets both).
-template <int D, int ITEMS>
+template <int D, int ITEMS, bool MERGED>
 __device__ __forceinline__ void sweep_uniform_ilp_body(const RoundParams& P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
@@ -536,7 +565,7 @@ __device__ __forceinline__ void sweep_uniform_ilp_body(const RoundParams& P) {
           for (int k = 0; k < ITEMS; ++k)
             if (live[k]) {
 #pragma unroll
-              for (int i = 0; i < D; ++i) cur[k][i] = ld_top(P, pv[k].v[i]);
+              for (int i = 0; i < D; ++i) cur[k][i] = ld_top_x<MERGED>(P, pv[k].v[i]);
             }
         }
 #pragma unroll
@@ -552,7 +581,7 @@ __device__ __forceinline__ void sweep_uniform_ilp_body(const RoundParams& P) {
             bool lost = false;
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-              tie |= deposit_key(P, pv[k].v[i], key[k], cur[k][i]);
+              tie |= deposit_key_x<MERGED>(P, pv[k].v[i], key[k], cur[k][i]);
               lost |= cur[k][i] > hi;
             }
             cand[k] = !lost;
@@ -881,7 +910,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
 // list id -> pins -> filter word are in flight per thread.
 constexpr int kCheckItems = 4;
 
-template <int D, bool STRIDED = false>
+template <int D, bool STRIDED = false, bool MERGED = false>
 __device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
   constexpr int ITEMS = D > 0 ? kCheckItems : 1;
   Ctrl* c = P.ctrl;
@@ -939,7 +968,7 @@ __device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
         // the edges sorted by first pin this load is nearly coalesced
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-          if (valid[k]) top0[k] = __ldcg(P.vtop + pv[k].v[0]);
+          if (valid[k]) top0[k] = MERGED ? __ldcg(top_half(P, pv[k].v[0])) : __ldcg(P.vtop + pv[k].v[0]);
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
           win[k] = false;
@@ -953,7 +982,7 @@ __device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
           if (win[k]) {
             uint32_t rest[D];
 #pragma unroll
-            for (int i = 1; i < D; ++i) rest[i] = __ldcg(P.vtop + pv[k].v[i]);
+            for (int i = 1; i < D; ++i) rest[i] = MERGED ? __ldcg(top_half(P, pv[k].v[i])) : __ldcg(P.vtop + pv[k].v[i]);
 #pragma unroll
             for (int i = 1; i < D; ++i) win[k] &= (rest[i] == static_cast<uint32_t>(key[k] >> 32));
           }
@@ -969,7 +998,7 @@ __device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
             if (win[k]) {
               mark_matched(P, e[k], r);
 #pragma unroll
-              for (int i = 0; i < D; ++i) mark_dead(P, pv[k].v[i]);
+              for (int i = 0; i < D; ++i) mark_dead_x<MERGED>(P, pv[k].v[i]);
               ++local_matched;
             }
           }
@@ -1224,10 +1253,18 @@ __global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_
 #else
 #define FUSED_MARK() do {} while (0)
 #endif
+  constexpr bool MERGED = !PIPE;  // (the pipelined sweep of d = 8 keeps the separate filter array)
   FUSED_MARK();
+  if (!X.init && MERGED) {
+    // a run continued here (after the host's exact redo of a tied round, a tag wrap, or the vertex-owned
+    // rounds of a handed-over run): covered vertices are known by the dead bitmap, which everyone maintains
+    for (uint32_t v = blockIdx.x * kBlock + threadIdx.x; v < P.n; v += gridDim.x * kBlock)
+      if ((__ldcg(P.dead + (v >> 5)) >> (v & 31u)) & 1u) P.vkey[v] = ~0ull;
+    grid.sync();
+  }
   if (X.init) {
     grid_zero(P.vkey, static_cast<size_t>(P.n) * 8);
-    grid_zero(P.vtop, static_cast<size_t>(P.n) * 4);
+    if (!MERGED) grid_zero(P.vtop, static_cast<size_t>(P.n) * 4);
     grid_zero(P.dead, ((static_cast<size_t>(P.n) + 31) / 32) * 4);
     grid_zero(P.mbits, static_cast<size_t>(X.mbits_words) * 4);
     grid_zero(P.matched_cnt, static_cast<size_t>(X.rounds_cap) * 4);
@@ -1239,11 +1276,11 @@ __global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_
   uint32_t status;
   for (;;) {
     if constexpr (PIPE) sweep_uniform_body<D, true, false, true>(P, nullptr);
-    else sweep_uniform_ilp_body<D, HLM_FUSED_ITEMS(D)>(P);
+    else sweep_uniform_ilp_body<D, HLM_FUSED_ITEMS(D), MERGED>(P);
     FUSED_MARK();
     grid.sync();
     FUSED_MARK();
-    check_commit_small_body<D, true>(P);
+    check_commit_small_body<D, true, MERGED>(P);
     FUSED_MARK();
     // the block that finishes the check last does the round bookkeeping: two grid barriers per round
     __syncthreads();
@@ -1259,6 +1296,10 @@ __global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_
     FUSED_MARK();
     status = *reinterpret_cast<volatile uint32_t*>(&P.ctrl->status);
     if (status != ST_RUNNING) break;
+  }
+  if (MERGED && (status == ST_TIE || status == ST_EPOCH)) {
+    // the host's kernels take the next step: give them the filter array they expect
+    for (uint32_t v = blockIdx.x * kBlock + threadIdx.x; v < P.n; v += gridDim.x * kBlock) P.vtop[v] = __ldcg(top_half(P, v));
   }
   if (!X.sum) return;
   const Ctrl* c = P.ctrl;
