@@ -1257,15 +1257,18 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   return HLM_B200_OK;
 }
 
-// Small uniform instances run all their rounds in one cooperative launch (k_rounds_fused) instead of the
-// CUDA graph: below ~8 M pins the three launches per round cost more than the round.  The limit is the pin
-// count of the whole instance (HLM_B200_FUSED_MAX_PINS overrides it; 0 disables the fused loop).
+// Small and mid-size uniform instances run all their rounds in one cooperative launch (k_rounds_fused) instead
+// of the CUDA graph.  d = 8 (pipelined sweep, separate filter array): up to 8 M pins, where the three launches
+// per round cost more than the round.  d = 2, 4 (filter word inside the 64-bit key, one atomic per pin): as
+// long as the n x 8 B of keys stay in L2, up to 64 M pins -- measured against the graph loop
+// (scripts/fused_limit_probe.py): 4-uniform 32 M pins 1.30 / 2.26 ms, 2-uniform 32 M pins 1.76 / 2.49 ms,
+// RMAT scale 20 with 2^24 edges 1.23 / 1.30 ms.  HLM_B200_FUSED_MAX_PINS replaces the limits (0: never).
 static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
   if (L.exact || g->num_large || g->fused_off) return false;
   if (g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
-  uint64_t limit = 1ull << 23;
-  if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) limit = std::strtoull(env, nullptr, 10);
-  return g->kappa <= limit;
+  if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) return g->kappa <= std::strtoull(env, nullptr, 10);
+  if (g->uniform_d == 8) return g->kappa <= (1ull << 23);
+  return g->kappa <= (1ull << 26) && static_cast<uint64_t>(g->n) * 8 <= static_cast<uint64_t>(g->l2_bytes);
 }
 
 static bool fused_pipelined(const Graph* g) {
