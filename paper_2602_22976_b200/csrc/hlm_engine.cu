@@ -1268,7 +1268,10 @@ static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
   if (g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
   if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) return g->kappa <= std::strtoull(env, nullptr, 10);
   if (g->uniform_d == 8) return g->kappa <= (1ull << 23);
-  return g->kappa <= (1ull << 26) && static_cast<uint64_t>(g->n) * 8 <= static_cast<uint64_t>(g->l2_bytes);
+  // dense instances (>= 6 pins per vertex: hubs, the load-before-atomic filter is on) gain less and lose to the
+  // specialised round-1 kernel of the graph loop from ~50 M pins on (RMAT scale 21, 2^25 edges: 1.71 / 1.51 ms)
+  const bool dense = g->kappa >= 6ull * g->n;
+  return g->kappa <= (dense ? 1ull << 25 : 1ull << 26) && static_cast<uint64_t>(g->n) * 8 <= static_cast<uint64_t>(g->l2_bytes);
 }
 
 static bool fused_pipelined(const Graph* g) {
@@ -1851,8 +1854,11 @@ bool crcw_is_faster(const Graph* g) {
   const uint64_t vtop_bytes = static_cast<uint64_t>(g->n) * 4, l2 = static_cast<uint64_t>(g->l2_bytes);
   // (8-uniform below ~4 M pins: the one-launch kernel of small instances, 0.27 against 0.34 ms at 2 M pins;
   // at 8 M pins the vertex-owned kernels are ahead again, 0.45 against 0.57 ms)
+  // (4-uniform: the one-launch kernel is ahead of the vertex-owned kernels while 8 B of key per vertex fill at
+  // most three quarters of L2 -- n = 10 M 1.72 / 1.93 ms, 12 M 2.24 / 2.29, 14 M 2.81 / 2.67)
   return g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
          (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4) ||
+         (g->uniform_d == 4 && !g->num_large && g->kappa <= (1ull << 26) && vtop_bytes * 2 <= l2 / 4 * 3) ||
          (g->uniform_d == 8 && !g->num_large && g->kappa <= (1ull << 22));
 }
 

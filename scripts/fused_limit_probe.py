@@ -9,11 +9,13 @@ def best(dg, variant, fused):
     cfg = hb.ParallelConfig(variant=variant)
     for _ in range(3): dg.match(ws, cfg)
     return min(dg.match(ws, cfg).report.device_ms for _ in range(10))
-cases = [("uniform", dict(n=4_000_000, m=8_000_000, d=2, seed=1)), ("uniform", dict(n=8_000_000, m=16_000_000, d=2, seed=1)),
-         ("uniform", dict(n=4_000_000, m=4_000_000, d=4, seed=1)), ("uniform", dict(n=8_000_000, m=8_000_000, d=4, seed=1)),
-         ("uniform", dict(n=16_000_000, m=16_000_000, d=4, seed=1)),
-         ("uniform", dict(n=1_000_000, m=2_000_000, d=8, seed=1)), ("uniform", dict(n=2_000_000, m=4_000_000, d=8, seed=1)),
-         ("rmat", dict(scale=20, m=1 << 24, seed=1, int_weights=True)), ("rmat", dict(scale=18, m=1 << 22, seed=1, int_weights=True))]
+cases = [("uniform", dict(n=10_000_000, m=10_000_000, d=4, seed=1)), ("uniform", dict(n=12_000_000, m=12_000_000, d=4, seed=1)),
+         ("uniform", dict(n=14_000_000, m=14_000_000, d=4, seed=1)), ("uniform", dict(n=6_000_000, m=16_000_000, d=4, seed=1)),
+         ("uniform", dict(n=12_000_000, m=24_000_000, d=2, seed=1)), ("uniform", dict(n=15_000_000, m=30_000_000, d=2, seed=1)),
+         ("uniform", dict(n=8_000_000, m=32_000_000, d=2, seed=1)), ("rmat", dict(scale=21, m=1 << 25, seed=1, int_weights=True)),
+         ("rmat", dict(scale=23, m=1 << 25, seed=1, int_weights=True))]
+if len(sys.argv) > 1:
+    cases = eval(sys.argv[1])
 for fam, spec in cases:
     dg = hb.DeviceHypergraph.generate(fam, **spec)
     info = dg.info()
