@@ -1264,9 +1264,11 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
 // (scripts/fused_limit_probe.py): 4-uniform 32 M pins 1.30 / 2.26 ms, 2-uniform 32 M pins 1.76 / 2.49 ms,
 // RMAT scale 20 with 2^24 edges 1.23 / 1.30 ms.  HLM_B200_FUSED_MAX_PINS replaces the limits (0: never).
 static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
-  if (L.exact || g->num_large || g->fused_off) return false;
-  if (g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
+  if (L.exact || g->fused_off || (g->num_large && g->uniform_d)) return false;
+  if (g->uniform_d != 0 && g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
   if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) return g->kappa <= std::strtoull(env, nullptr, 10);
+  if (g->uniform_d == 0)  // ragged sizes: the plain sweeps (thread per edge, warp per large edge), filter word in the key
+    return g->kappa <= (1ull << 23) && static_cast<uint64_t>(g->n) * 8 <= static_cast<uint64_t>(g->l2_bytes);
   if (g->uniform_d == 8) return g->kappa <= (1ull << 23);
   // dense instances (>= 6 pins per vertex: hubs, the load-before-atomic filter is on) gain less and lose to the
   // specialised round-1 kernel of the graph loop from ~50 M pins on (RMAT scale 21, 2^25 edges: 1.71 / 1.51 ms)
@@ -1275,6 +1277,7 @@ static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
 }
 
 static bool fused_pipelined(const Graph* g) {
+  if (g->uniform_d == 0) return false;
   if (const char* env = std::getenv("HLM_B200_FUSED_PIPE")) return env[0] == '1';
   return g->uniform_d == 8;  // measured (scripts/fused_tune.sh): d = 8 gains 11 %, d = 2, 4 lose 5-10 %
 }
@@ -1288,6 +1291,7 @@ static const void* fused_kernel(const Graph* g) {
     }
   }
   switch (g->uniform_d) {
+    case 0: return reinterpret_cast<const void*>(&k_rounds_fused<0, false>);
     case 2: return reinterpret_cast<const void*>(&k_rounds_fused<2, false>);
     case 4: return reinterpret_cast<const void*>(&k_rounds_fused<4, false>);
     default: return reinterpret_cast<const void*>(&k_rounds_fused<8, false>);
@@ -1369,7 +1373,7 @@ static int fused_prepare(Graph* g, const hlm_b200_config* cfg, const Ctrl& c0, F
     ST_CHECK(dev_alloc(&w.fused_block_isum, static_cast<size_t>(g->fused_grid), g));
   }
   if (!w.fused_sum) CU_CHECK(cudaHostAlloc(&w.fused_sum, sizeof(FusedSummary), cudaHostAllocDefault));
-  const uint64_t bound = std::min<uint64_t>(g->m, g->n / g->uniform_d);  // matched edges are disjoint
+  const uint64_t bound = std::min<uint64_t>(g->m, g->uniform_d ? g->n / g->uniform_d : g->n);  // matched edges are disjoint
   const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
   if (bound + 8 > w.out_cap) {  // device staging of the result (shared with the usual assembly)
     dev_free(w.out_ids);
@@ -1859,6 +1863,9 @@ bool crcw_is_faster(const Graph* g) {
   return g->m < (1u << 16) || (g->uniform_d == 2 && vtop_bytes <= l2) ||
          (g->uniform_d > 2 && g->uniform_d <= 4 && vtop_bytes <= l2 / 4) ||
          (g->uniform_d == 4 && !g->num_large && g->kappa <= (1ull << 26) && vtop_bytes * 2 <= l2 / 4 * 3) ||
+         // small ragged instances without very long edges: the one-launch kernel (power-law 6 M pins 0.59 against
+         // 0.79 ms, sizes 2..8 5 M pins 0.43 / 0.46; nets of thousands of pins want the vertex-owned tasks: 0.59 / 0.47)
+         (g->uniform_d == 0 && g->kappa <= (1ull << 23) && vtop_bytes * 2 <= l2 && g->max_edge_size <= 256) ||
          (g->uniform_d == 8 && !g->num_large && g->kappa <= (1ull << 22));
 }
 

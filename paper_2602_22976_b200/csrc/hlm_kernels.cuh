@@ -70,6 +70,35 @@ __device__ __forceinline__ bool span_all_dead(const RoundParams& P, uint32_t fir
   return __all_sync(0xffffffffu, ok);
 }
 
+// MERGED (fused kernel, d = 2 / 4): the filter word of a vertex is the high half of its 64-bit key in place --
+// no second array and no second atomic per deposit.  An instance this small keeps vkey (8 B per vertex) in L2,
+// which is what the separate 4-byte array exists for elsewhere; round 1 of config 1 is bound by the L2's
+// atomic rate (8 M atomicMax -> 4 M: 50 -> 27 us).  A covered vertex holds all-ones in both halves.
+__device__ __forceinline__ const uint32_t* top_half(const RoundParams& P, uint32_t v) {
+  return reinterpret_cast<const uint32_t*>(P.vkey + v) + 1;  // little-endian: the high word
+}
+template <bool MERGED>
+__device__ __forceinline__ uint32_t ld_top_x(const RoundParams& P, uint32_t v) {
+  if constexpr (!MERGED) return ld_top(P, v);
+  else return v < P.hot_vtop ? __ldca(top_half(P, v)) : __ldcg(top_half(P, v));
+}
+template <bool MERGED>
+__device__ __forceinline__ bool deposit_key_x(const RoundParams& P, uint32_t v, unsigned long long key, uint32_t cur) {
+  if constexpr (!MERGED) return deposit_key(P, v, key, cur);
+  else {
+    if (cur > static_cast<uint32_t>(key >> 32)) return false;
+    return atomicMax(P.vkey + v, key) == key;
+  }
+}
+template <bool MERGED>
+__device__ __forceinline__ void mark_dead_x(const RoundParams& P, uint32_t v) {
+  if constexpr (!MERGED) mark_dead(P, v);
+  else {
+    P.vkey[v] = ~0ull;
+    atomicOr(P.dead + (v >> 5), 1u << (v & 31));
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Round sweep, uniform edge size D (2, 4, 8): one thread per edge, one 64/128-bit pin load per
 // edge, software-pipelined over the 32-edge batches of a warp's region.
@@ -459,35 +488,6 @@ __device__ __forceinline__ void sweep_uniform_simple_body(const RoundParams& P) 
   if (tie) c->tie_flag = 1u;
 }
 
-// MERGED (fused kernel, d = 2 / 4): the filter word of a vertex is the high half of its 64-bit key in place --
-// no second array and no second atomic per deposit.  An instance this small keeps vkey (8 B per vertex) in L2,
-// which is what the separate 4-byte array exists for elsewhere; round 1 of config 1 is bound by the L2's
-// atomic rate (8 M atomicMax -> 4 M: 50 -> 27 us).  A covered vertex holds all-ones in both halves.
-__device__ __forceinline__ const uint32_t* top_half(const RoundParams& P, uint32_t v) {
-  return reinterpret_cast<const uint32_t*>(P.vkey + v) + 1;  // little-endian: the high word
-}
-template <bool MERGED>
-__device__ __forceinline__ uint32_t ld_top_x(const RoundParams& P, uint32_t v) {
-  if constexpr (!MERGED) return ld_top(P, v);
-  else return v < P.hot_vtop ? __ldca(top_half(P, v)) : __ldcg(top_half(P, v));
-}
-template <bool MERGED>
-__device__ __forceinline__ bool deposit_key_x(const RoundParams& P, uint32_t v, unsigned long long key, uint32_t cur) {
-  if constexpr (!MERGED) return deposit_key(P, v, key, cur);
-  else {
-    if (cur > static_cast<uint32_t>(key >> 32)) return false;
-    return atomicMax(P.vkey + v, key) == key;
-  }
-}
-template <bool MERGED>
-__device__ __forceinline__ void mark_dead_x(const RoundParams& P, uint32_t v) {
-  if constexpr (!MERGED) mark_dead(P, v);
-  else {
-    P.vkey[v] = ~0ull;
-    atomicOr(P.dead + (v >> 5), 1u << (v & 31));
-  }
-}
-
 // The sweep of the fused small-instance kernel: the same decisions as the plain sweep, ITEMS batches of a
 // region per step with the loads of all of them issued together.  A small instance is latency-bound -- the
 // resident warps each walk a few batches one dependent L2 round trip after the other (config 1: 6.6 batches
@@ -754,8 +754,8 @@ __global__ void __launch_bounds__(kBlock, HLM_SIMPLE_MIN_BLOCKS) k_sweep_uniform
 // Round sweep, runtime edge sizes (<= kLargeEdge pins per edge): one thread per short edge, the
 // whole warp for a medium one.
 // ---------------------------------------------------------------------------------------------
-template <bool VMAX>
-__global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(const RoundParams P) {
+template <bool VMAX, bool STRIDED = false, bool MERGED = false>
+__device__ __forceinline__ void filter_vmax_small_body(const RoundParams& P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -774,9 +774,15 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
   const bool dead_first = r > 1 && P.dead_first;
 
   const uint32_t gran = claim_granularity(P, c->active_prev);
+  uint32_t next_claim = grid_warp();
   for (uint32_t seg = 0, seg_end = 0;; ++seg) {
     if (seg == seg_end) {
-      seg = claim_region(&c->ticket_f, lane, false) * gran;
+      if constexpr (STRIDED) {
+        seg = next_claim * gran;
+        next_claim += gridDim.x * kWarpsPerBlock;
+      } else {
+        seg = claim_region(&c->ticket_f, lane, false) * gran;
+      }
       seg_end = seg + gran;
     }
     if (seg >= P.nseg) break;
@@ -787,7 +793,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
       const uint32_t idx = t0 + lane;
       bool survive = idx < cnt, cand = false;
       uint32_t e = 0;
-      if (survive) e = in_ident ? seg_base + idx : in[seg_base + idx];
+      if (survive) e = in_ident ? seg_base + idx : __ldcg(in + seg_base + idx);
       bool is_long = false;
       uint64_t long_b = 0;
       uint32_t long_s = 0;
@@ -814,7 +820,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              cur[i] = (peek && !dead_any && static_cast<uint32_t>(i) < s) ? ld_top(P, v[i]) : 0u;
+              cur[i] = (peek && !dead_any && static_cast<uint32_t>(i) < s) ? ld_top_x<MERGED>(P, v[i]) : 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) dead_any |= (static_cast<uint32_t>(i) < s && cur[i] == kTopDead);
             if (dead_any) {
@@ -828,7 +834,7 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
 #pragma unroll
               for (int i = 0; i < 8; ++i)
                 if (static_cast<uint32_t>(i) < s) {
-                  tie |= deposit_key(P, v[i], key, cur[i]);
+                  tie |= deposit_key_x<MERGED>(P, v[i], key, cur[i]);
                   lost |= cur[i] > hi;
                 }
               cand = !lost;
@@ -853,13 +859,13 @@ __global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(co
         const uint32_t v = mine ? __ldg(P.csr.pins + eb + lane) : 0u;
         const bool peek = r > 1 || P.ks.precheck;
         bool dead_any = dead_first && __any_sync(0xffffffffu, mine && is_dead(P, v));
-        const uint32_t cur = (mine && peek && !dead_any) ? ld_top(P, v) : 0u;
+        const uint32_t cur = (mine && peek && !dead_any) ? ld_top_x<MERGED>(P, v) : 0u;
         dead_any = dead_any || __any_sync(0xffffffffu, mine && cur == kTopDead);
         bool lost = false;
         if (!dead_any) {
           if constexpr (VMAX) {
             const unsigned long long key = priority_key(P.stream, P.ks, edge_gid(P, ee), r, base_of(P, ee), tag);
-            if (mine) tie |= deposit_key(P, v, key, cur);
+            if (mine) tie |= deposit_key_x<MERGED>(P, v, key, cur);
             lost = __any_sync(0xffffffffu, mine && cur > static_cast<uint32_t>(key >> 32));
           }
         }
@@ -1012,12 +1018,13 @@ __device__ __forceinline__ void check_commit_small_body(const RoundParams& P) {
             const unsigned long long key =
                 priority_key(P.stream, P.ks, edge_gid(P, e[0]), r, base_of(P, e[0]), tag);
             bool w = true;
-            for (uint32_t i = 0; i < s && w; ++i) w = key_wins_at(P, __ldg(pp + i), key);
+            for (uint32_t i = 0; i < s && w; ++i)
+              w = MERGED ? __ldcg(P.vkey + __ldg(pp + i)) == key : key_wins_at(P, __ldg(pp + i), key);
             if (w) {
               mark_matched(P, e[0], r);
               for (uint32_t i = 0; i < s; ++i) {
                 const uint32_t v = __ldg(pp + i);
-                mark_dead(P, v);
+                mark_dead_x<MERGED>(P, v);
               }
               ++local_matched;
               local_mpins += s;
@@ -1050,7 +1057,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_check_commit_small(const RoundPar
 enum LargeState : uint8_t { LARGE_DROPPED = 0, LARGE_ACTIVE = 1, LARGE_CANDIDATE = 2 };
 
 template <bool VMAX>
-__global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams P) {
+__global__ void __launch_bounds__(kBlock, HLM_MIN_BLOCKS) k_filter_vmax_small(const RoundParams P) {
+  filter_vmax_small_body<VMAX>(P);
+}
+template <bool VMAX, bool MERGED = false>
+__device__ __forceinline__ void filter_vmax_large_body(const RoundParams& P) {
   Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   const uint32_t par = c->parity;
@@ -1088,7 +1099,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
         bool d = false;
         if (i < s) {
           const uint32_t v = __ldg(pp + i);
-          d = use_bits ? is_dead(P, v) : (__ldcg(P.vtop + v) == kTopDead);
+          d = use_bits ? is_dead(P, v) : (ld_top_x<MERGED>(P, v) == kTopDead);
         }
         dead_any = __any_sync(0xffffffffu, d);
       }
@@ -1107,8 +1118,8 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
     if constexpr (VMAX) {
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
-        const uint32_t cur = __ldcg(P.vtop + v);
-        tie |= deposit_key(P, v, key, cur);
+        const uint32_t cur = MERGED ? __ldcg(top_half(P, v)) : __ldcg(P.vtop + v);
+        tie |= deposit_key_x<MERGED>(P, v, key, cur);
         lost |= cur > hi;
       }
       lost = __any_sync(0xffffffffu, lost);
@@ -1122,7 +1133,13 @@ __global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams 
   if (tie) c->tie_flag = 1u;
 }
 
-__global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams P) {
+template <bool VMAX>
+__global__ void __launch_bounds__(kBlock) k_filter_vmax_large(const RoundParams P) {
+  filter_vmax_large_body<VMAX>(P);
+}
+
+template <bool MERGED = false>
+__device__ __forceinline__ void check_commit_large_body(const RoundParams& P) {
   const Ctrl* c = P.ctrl;
   const uint32_t r = c->round;
   if (c->tie_flag || r > c->max_rounds) return;
@@ -1149,14 +1166,14 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
     bool win = true;
     for (uint32_t i0 = 0; i0 < s; i0 += 32) {
       const uint32_t i = i0 + lane;
-      const bool ok = i < s ? key_wins_at(P, __ldg(pp + i), key) : true;
+      const bool ok = i < s ? (MERGED ? __ldcg(P.vkey + __ldg(pp + i)) == key : key_wins_at(P, __ldg(pp + i), key)) : true;
       win = __all_sync(0xffffffffu, ok);
       if (!win) break;  // first losing chunk ends the scan
     }
     if (win) {
       for (uint32_t i = lane; i < s; i += 32) {
         const uint32_t v = __ldg(pp + i);
-        mark_dead(P, v);
+        mark_dead_x<MERGED>(P, v);
       }
       if (lane == 0) {
         mark_matched(P, e, r);
@@ -1169,6 +1186,8 @@ __global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams
   if (local_matched) atomicAdd(P.matched_cnt + r, local_matched);
   if (local_mpins) atomicAdd(&P.ctrl->pins_matched, local_mpins);
 }
+
+__global__ void __launch_bounds__(kBlock) k_check_commit_large(const RoundParams P) { check_commit_large_body<>(P); }
 
 // One thread.  Round bookkeeping between check/commit of round r and the filter of round r+1;
 // sets the WHILE condition of the enclosing CUDA graph when there is one.
@@ -1269,18 +1288,26 @@ __global__ void __launch_bounds__(kBlock, PIPE ? (D == 8 ? 2 : 3) : 4) k_rounds_
     grid_zero(P.mbits, static_cast<size_t>(X.mbits_words) * 4);
     grid_zero(P.matched_cnt, static_cast<size_t>(X.rounds_cap) * 4);
     grid_zero(P.deact_cnt, static_cast<size_t>(X.rounds_cap) * 4);
+    for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < P.num_large; i += gridDim.x * kBlock) P.large_state[i] = LARGE_ACTIVE;
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctrl = X.c0;
     grid.sync();
     FUSED_MARK();
   }
   uint32_t status;
   for (;;) {
-    if constexpr (PIPE) sweep_uniform_body<D, true, false, true>(P, nullptr);
+    if constexpr (D == 0) {  // ragged sizes; the (few) edges above kLargeEdge pins by whole warps in the same phase
+      filter_vmax_small_body<true, true, MERGED>(P);
+      if (P.num_large) filter_vmax_large_body<true, MERGED>(P);
+    }
+    else if constexpr (PIPE) sweep_uniform_body<D, true, false, true>(P, nullptr);
     else sweep_uniform_ilp_body<D, HLM_FUSED_ITEMS(D), MERGED>(P);
     FUSED_MARK();
     grid.sync();
     FUSED_MARK();
     check_commit_small_body<D, true, MERGED>(P);
+    if constexpr (D == 0) {
+      if (P.num_large) check_commit_large_body<MERGED>(P);
+    }
     FUSED_MARK();
     // the block that finishes the check last does the round bookkeeping: two grid barriers per round
     __syncthreads();

@@ -1,4 +1,4 @@
-"""The one-launch kernel of small uniform instances (k_rounds_fused): initialisation,
+"""The one-launch kernel of small instances (uniform d = 2 / 4 / 8, or ragged sizes: k_rounds_fused): initialisation,
 every round and the result assembly in one cooperative launch.  It must give what the oracle gives --
 matching, rounds, per-round counts, total weight -- on every path through it: integer weights (summed on the
 device), unit weights, real weights (assembly on the usual path), ties (the kernel hands the round to the
@@ -13,6 +13,11 @@ from tests.util import assert_same_result, to_hb_graph, to_hb_stream
 pytestmark = pytest.mark.gpu
 
 
+def _weighted(port, g):
+    g.base_weights = port.random_weights_1_100(g.m, 3)
+    return g
+
+
 def _cases(port):
     yield "4-uniform, unit weights", port.generate_random(30_000, 30_000, 4, 4, 1), True
     yield "2-uniform graph, weights 1-100", port.syn_generate(po.SYN_RMAT, scale=13, m=60_000, seed=2, int_weights=True), True
@@ -22,7 +27,11 @@ def _cases(port):
     real.base_weights[:] = 0.25 + np.random.default_rng(11).random(real.m) * 7.5
     yield "4-uniform, real weights", real, None
     yield "one edge", port.generate_random(4, 1, 4, 4, 1), True
-    yield "ragged 2..5 (not eligible)", port.generate_random(2000, 3500, 2, 5, 7), False
+    yield "ragged 2..5", port.generate_random(2000, 3500, 2, 5, 7), True
+    yield "ragged 1..30, weights 1-100", _weighted(port, port.generate_random(30_000, 20_000, 1, 30, 5)), True
+    yield "power-law 2..64 (edges above 32 pins: warp per edge)", port.syn_generate(po.SYN_POWERLAW, n=4000, m=6000, seed=5), True
+    yield "netlist <= 4096, weights 1-100", port.syn_generate(po.SYN_NETLIST, n=9000, m=12000, seed=6, int_weights=True), True
+    yield "3-uniform (not eligible: no kernel for d = 3)", port.generate_random(3000, 4000, 3, 3, 2), False
 
 
 STREAMS = [po.Stream(seed=1), po.Stream(seed=4, noise_high=0.0),  # every key of a weight class ties
