@@ -1257,6 +1257,9 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
   return HLM_B200_OK;
 }
 
+// the ragged form of the one-launch kernel also serves uniform sizes other than 2 / 4 / 8
+static bool fused_generic(const Graph* g) { return g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8; }
+
 // Small and mid-size uniform instances run all their rounds in one cooperative launch (k_rounds_fused) instead
 // of the CUDA graph.  d = 8 (pipelined sweep, separate filter array): up to 8 M pins, where the three launches
 // per round cost more than the round.  d = 2, 4 (filter word inside the 64-bit key, one atomic per pin): as
@@ -1264,10 +1267,9 @@ static int setup_launcher(Graph* g, const hlm_b200_stream* st, const hlm_b200_co
 // (scripts/fused_limit_probe.py): 4-uniform 32 M pins 1.30 / 2.26 ms, 2-uniform 32 M pins 1.76 / 2.49 ms,
 // RMAT scale 20 with 2^24 edges 1.23 / 1.30 ms.  HLM_B200_FUSED_MAX_PINS replaces the limits (0: never).
 static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
-  if (L.exact || g->fused_off || (g->num_large && g->uniform_d)) return false;
-  if (g->uniform_d != 0 && g->uniform_d != 2 && g->uniform_d != 4 && g->uniform_d != 8) return false;
+  if (L.exact || g->fused_off || (g->num_large && !fused_generic(g))) return false;
   if (const char* env = std::getenv("HLM_B200_FUSED_MAX_PINS")) return g->kappa <= std::strtoull(env, nullptr, 10);
-  if (g->uniform_d == 0)  // ragged sizes: the plain sweeps (thread per edge, warp per large edge), filter word in the key
+  if (fused_generic(g))  // ragged sizes (or uniform ones other than 2 / 4 / 8): the plain sweeps (thread per edge, warp per large edge), filter word in the key
     return g->kappa <= (1ull << 23) && static_cast<uint64_t>(g->n) * 8 <= static_cast<uint64_t>(g->l2_bytes);
   if (g->uniform_d == 8) return g->kappa <= (1ull << 23);
   // dense instances (>= 6 pins per vertex: hubs, the load-before-atomic filter is on) gain less and lose to the
@@ -1277,7 +1279,7 @@ static bool fused_rounds_ok(const Graph* g, const Launcher& L) {
 }
 
 static bool fused_pipelined(const Graph* g) {
-  if (g->uniform_d == 0) return false;
+  if (fused_generic(g)) return false;
   if (const char* env = std::getenv("HLM_B200_FUSED_PIPE")) return env[0] == '1';
   return g->uniform_d == 8;  // measured (scripts/fused_tune.sh): d = 8 gains 11 %, d = 2, 4 lose 5-10 %
 }
@@ -1291,10 +1293,10 @@ static const void* fused_kernel(const Graph* g) {
     }
   }
   switch (g->uniform_d) {
-    case 0: return reinterpret_cast<const void*>(&k_rounds_fused<0, false>);
     case 2: return reinterpret_cast<const void*>(&k_rounds_fused<2, false>);
     case 4: return reinterpret_cast<const void*>(&k_rounds_fused<4, false>);
-    default: return reinterpret_cast<const void*>(&k_rounds_fused<8, false>);
+    case 8: return reinterpret_cast<const void*>(&k_rounds_fused<8, false>);
+    default: return reinterpret_cast<const void*>(&k_rounds_fused<0, false>);  // ragged, or uniform of another size
   }
 }
 

@@ -31,7 +31,8 @@ def _cases(port):
     yield "ragged 1..30, weights 1-100", _weighted(port, port.generate_random(30_000, 20_000, 1, 30, 5)), True
     yield "power-law 2..64 (edges above 32 pins: warp per edge)", port.syn_generate(po.SYN_POWERLAW, n=4000, m=6000, seed=5), True
     yield "netlist <= 4096, weights 1-100", port.syn_generate(po.SYN_NETLIST, n=9000, m=12000, seed=6, int_weights=True), True
-    yield "3-uniform (not eligible: no kernel for d = 3)", port.generate_random(3000, 4000, 3, 3, 2), False
+    yield "3-uniform (the ragged form)", port.generate_random(3000, 4000, 3, 3, 2), True
+    yield "40-uniform (every edge a warp's)", port.generate_random(30_000, 2000, 40, 40, 2), True
 
 
 STREAMS = [po.Stream(seed=1), po.Stream(seed=4, noise_high=0.0),  # every key of a weight class ties
