@@ -232,7 +232,7 @@ void Workspace::release() {
   dev_free(int_sum);
   dev_free(fused_block_cnt);
   dev_free(fused_block_isum);
-  if (fused_sum) cudaFreeHost(fused_sum);
+  host_result_free(fused_sum);
   if (pin_w) cudaFreeHost(pin_w);
   drop_graphs();
   if (ev0) cudaEventDestroy(ev0);
@@ -1374,7 +1374,15 @@ static int fused_prepare(Graph* g, const hlm_b200_config* cfg, const Ctrl& c0, F
     ST_CHECK(dev_alloc(&w.fused_block_cnt, static_cast<size_t>(g->fused_grid), g));
     ST_CHECK(dev_alloc(&w.fused_block_isum, static_cast<size_t>(g->fused_grid), g));
   }
-  if (!w.fused_sum) CU_CHECK(cudaHostAlloc(&w.fused_sum, sizeof(FusedSummary), cudaHostAllocDefault));
+  if (!w.fused_sum) {  // from the page-locked pool: a one-shot call (hlm_b200_match_host) must not pay cudaHostAlloc / cudaFreeHost
+    w.fused_sum = static_cast<FusedSummary*>(host_result_alloc(sizeof(FusedSummary)));
+    if (!w.fused_sum || !host_result_pinned(w.fused_sum)) {
+      host_result_free(w.fused_sum);
+      w.fused_sum = nullptr;
+      return HLM_B200_OK;
+    }
+    std::memset(w.fused_sum, 0, sizeof(FusedSummary));
+  }
   const uint64_t bound = std::min<uint64_t>(g->m, g->uniform_d ? g->n / g->uniform_d : g->n);  // matched edges are disjoint
   const bool want_round = !(cfg->flags & HLM_B200_FLAG_NO_ROUND_OF);
   if (bound + 8 > w.out_cap) {  // device staging of the result (shared with the usual assembly)
