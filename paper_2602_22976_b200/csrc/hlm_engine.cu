@@ -1456,6 +1456,7 @@ static int crcw_run(Graph* g, Launcher& L, uint32_t max_rounds, bool use_graph, 
         if (g->fused_off) {  // refused: nothing ran; the state reset the kernel would have done, then the graph loop
           if (S.fused && S.fused->init) ST_CHECK(reset_match_state(g, S.fused->c0));
           S.fused = nullptr;
+          if (w.graph_exec[0] && !same_params(w.graph_key, L.P)) w.drop_graphs();  // graphs of an earlier stream / config
           continue;
         }
         ++graph_launches;
@@ -1578,7 +1579,11 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   }
 
   bool use_graph = cfg->loop_mode != HLM_B200_LOOP_HOST && !L.exact;
-  if (use_graph && (!w.graph_exec[0] || !same_params(w.graph_key, P))) {
+  const bool fused = use_graph && g->m && !greedy && fused_rounds_ok(g, L);
+  // an instance that lives for one matching (hlm_b200_match_host): building the CUDA graph (0.3 ms) costs more
+  // than the host loop's per-round synchronisations save; the one-launch kernel needs no graph
+  if (g->one_shot && cfg->loop_mode == HLM_B200_LOOP_AUTO && !fused) use_graph = false;
+  if (use_graph && !fused && (!w.graph_exec[0] || !same_params(w.graph_key, P))) {
     w.drop_graphs();
     ST_CHECK(build_loop_graph(L, 0));
   }
@@ -1598,7 +1603,7 @@ int match_crcw(Graph* g, const hlm_b200_stream* st, const hlm_b200_config* cfg, 
   PreAssembled pre;
   bool fused_all = false;
   std::memset(&fx, 0, sizeof(fx));
-  if (use_graph && g->m && !greedy && fused_rounds_ok(g, L)) ST_CHECK(fused_prepare(g, cfg, c0, &fx, &pre, &fused_all));
+  if (fused) ST_CHECK(fused_prepare(g, cfg, c0, &fx, &pre, &fused_all));
   if (!fused_all) ST_CHECK(reset_match_state(g, c0));
 
   Ctrl c = c0;
@@ -2211,11 +2216,7 @@ int hlm_b200_match_host(const hlm_b200_csr_view* host, const hlm_b200_stream* st
   if (rc != HLM_B200_OK) return rc;
   g->one_shot = true;
   tr.mark("match_host: upload");
-  // a single matching: building the CUDA graph (0.3 ms) costs more than the host loop's per-round
-  // synchronisations save
-  hlm_b200_config one_shot = *cfg;
-  if (one_shot.loop_mode == HLM_B200_LOOP_AUTO) one_shot.loop_mode = HLM_B200_LOOP_HOST;
-  cfg = &one_shot;
+  // (a single matching: match_crcw takes the one-launch kernel where it applies, else the host-driven loop)
   rc = run_match(g, stream, cfg, out);
   tr.mark("match_host: match");
   out->h2d_bytes = g->h2d_bytes;
