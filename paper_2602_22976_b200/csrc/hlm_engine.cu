@@ -448,7 +448,35 @@ struct HostScan {
   std::atomic<uint64_t> next{0};
   std::atomic<bool> nonuniform{false};
   std::atomic<bool> nopack{false};
+  // ragged instances: 16-bit edge sizes (page-locked, 2 bytes per edge) go up instead of the 64-bit offsets
+  uint16_t* sizes = nullptr;
+  std::atomic<bool> nosizes{false};
+  std::unique_ptr<std::atomic<uint8_t>[]> sized;  // [offset chunk] its sizes are written
+  ~HostScan() {
+    if (packed) host_result_free(packed);
+    if (sizes) host_result_free(sizes);
+  }
   static constexpr uint64_t kChunk = 1ull << 20;
+  // one chunk of offsets: uniform so far -> compare with d0; ragged (known, or found out here) -> pack the sizes
+  void offsets_chunk(uint64_t c, uint64_t b, uint64_t e) {
+    if (!nonuniform.load(std::memory_order_relaxed) && host_offsets_differ(off, d0, b, e))
+      nonuniform.store(true, std::memory_order_relaxed);
+    if (nonuniform.load(std::memory_order_relaxed) && sizes && !nosizes.load(std::memory_order_relaxed)) {
+      if (host_pack_sizes_u16(off, sizes, b, e)) nosizes.store(true, std::memory_order_relaxed);
+      sized[c].store(1, std::memory_order_release);
+    }
+  }
+  // after every chunk was looked at: the chunks that passed as uniform before the instance turned out ragged
+  bool finish_sizes() {
+    if (!sizes || nosizes.load() || !nonuniform.load()) return false;
+    const uint64_t nc = chunks_per_array();
+    for (uint64_t c = 0; c < nc; ++c)
+      if (!sized[c].load(std::memory_order_acquire)) {
+        const uint64_t b = c * kChunk, e = std::min(m, b + kChunk);
+        if (host_pack_sizes_u16(off, sizes, b, e)) return false;
+      }
+    return !nosizes.load();
+  }
   uint64_t chunks_per_array() const { return (m + kChunk - 1) / kChunk; }
   std::atomic<uint64_t> weight_chunks_done{0};
   // Weight chunks come first in the queue: the packed bytes are ready well before the pins have
@@ -464,8 +492,7 @@ struct HostScan {
       const bool is_off = t >= nc;
       const uint64_t b = (is_off ? t - nc : t) * kChunk, e = std::min(m, b + kChunk);
       if (is_off) {
-        if (nonuniform.load(std::memory_order_relaxed)) continue;
-        if (host_offsets_differ(off, d0, b, e)) nonuniform.store(true, std::memory_order_relaxed);
+        offsets_chunk(t - nc, b, e);
       } else {
         if (!nopack.load(std::memory_order_relaxed)) {
           if (host_pack_weights_u8(w, packed, b, e)) nopack.store(true, std::memory_order_relaxed);
@@ -483,8 +510,7 @@ struct HostScan {
     const bool is_off = t >= nc;
     const uint64_t b = (is_off ? t - nc : t) * kChunk, e = std::min(m, b + kChunk);
     if (is_off) {
-      if (!nonuniform.load(std::memory_order_relaxed) && host_offsets_differ(off, d0, b, e))
-        nonuniform.store(true, std::memory_order_relaxed);
+      offsets_chunk(t - nc, b, e);
     } else {
       if (!nopack.load(std::memory_order_relaxed) && host_pack_weights_u8(w, packed, b, e))
         nopack.store(true, std::memory_order_relaxed);
@@ -656,6 +682,15 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
     scan.packed = static_cast<uint8_t*>(host_result_alloc(m));
     if (!scan.packed) scan.nopack = true;
     if (scan.d0 == 0 || scan.d0 > kLargeEdge) scan.nonuniform = true;  // plain path handles these
+    // (only where the first edges already differ in size: a uniform instance needs no buffer, and one that
+    // turns ragged later takes the plain offset copy as before)
+    if (!std::getenv("HLM_B200_NO_SIZE_PACK") &&
+        (scan.nonuniform.load() || host_offsets_differ(h->edge_offsets, scan.d0, 0, std::min<uint64_t>(m, 1u << 16)))) {
+      scan.sizes = static_cast<uint16_t*>(host_result_alloc(static_cast<size_t>(m) * 2));
+      scan.sized.reset(new std::atomic<uint8_t>[scan.chunks_per_array()]);
+      for (uint64_t c = 0; c < scan.chunks_per_array(); ++c) scan.sized[c].store(0, std::memory_order_relaxed);
+      if (!scan.sizes) scan.nosizes = true;
+    }
   }
   cudaError_t e = cudaSuccess;
   // The pins go up in 256 MB pieces; a second stream takes the largest vertex id of every piece
@@ -833,17 +868,44 @@ static int upload(const hlm_b200_csr_view* h, int device, Graph** out, const Upl
   } else {
     uint64_t* off64 = nullptr;
     if ((rc = dev_alloc(&off64, static_cast<size_t>(m) + 1, nullptr)) != HLM_B200_OK) return fail(rc);
-    if (m) {
+    // ragged: the host packed the edge sizes into 16 bits while the pins went up (2 instead of 8 bytes per edge
+    // over PCIe, and from page-locked memory whatever the caller's arrays are); the offsets are their scan
+    bool from_sizes = assist && m && scan.finish_sizes();
+    if (from_sizes) {
+      uint16_t* d16 = nullptr;
+      uint32_t* d32 = nullptr;
+      uint64_t total = 0;
+      rc = dev_alloc(&d16, m, nullptr);
+      if (rc == HLM_B200_OK) rc = dev_alloc(&d32, m, nullptr);
+      if (rc == HLM_B200_OK) {
+        e = cudaMemcpyAsync(d16, scan.sizes, static_cast<size_t>(m) * 2, cudaMemcpyHostToDevice, s);
+        k_widen_sizes<<<grid_for(g, m), kBlock, 0, s>>>(d16, d32, m);
+        if (e == cudaSuccess) rc = device_exclusive_scan_u32_to_u64(g, d32, off64, m, &total);
+      }
+      pool_free(d16);
+      pool_free(d32);
+      if (rc != HLM_B200_OK || e != cudaSuccess || total != g->kappa) {
+        cudaGetLastError();
+        from_sizes = false;  // whatever went wrong: the plain copy below is always right
+        rc = HLM_B200_OK;
+        e = cudaSuccess;
+      } else {
+        g->h2d_bytes += static_cast<uint64_t>(m) * 2;
+      }
+    }
+    if (m && !from_sizes) {
       e = cudaMemcpyAsync(off64, h->edge_offsets, (static_cast<size_t>(m) + 1) * 8, cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) {
         set_error("host-to-device copy failed: %s", cudaGetErrorString(e));
         pool_free(off64);
         return fail(HLM_B200_ERR_CUDA);
       }
+      g->h2d_bytes += (static_cast<uint64_t>(m) + 1) * 8;
     }
-    g->h2d_bytes += (static_cast<uint64_t>(m) + 1) * 8;
     if ((rc = finish_graph(g, off64, true)) != HLM_B200_OK) return fail(rc);
   }
+  if (scan.sizes) host_result_free(scan.sizes);
+  scan.sizes = nullptr;
   tr.mark("upload: edge structure");
   if ((rc = finish_weights(g, code_stats_queued ? &code_ws : nullptr)) != HLM_B200_OK) return fail(rc);
   tr.mark("upload: weight stats");

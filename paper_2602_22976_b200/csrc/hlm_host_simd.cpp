@@ -21,6 +21,16 @@ bool host_pack_weights_u8_scalar(const double* w, uint8_t* packed, uint64_t b, u
   return bad;
 }
 
+bool host_pack_sizes_u16(const uint64_t* off, uint16_t* sizes, uint64_t b, uint64_t e) {
+  uint64_t high = 0;
+  for (uint64_t i = b; i < e; ++i) {
+    const uint64_t d = off[i + 1] - off[i];  // decreasing offsets wrap to a huge value
+    high |= d;
+    sizes[i] = static_cast<uint16_t>(d);
+  }
+  return (high >> 16) != 0;
+}
+
 bool host_offsets_differ_scalar(const uint64_t* off, uint64_t d, uint64_t b, uint64_t e) {
   uint64_t bad = 0;
   for (uint64_t i = b; i < e; ++i) bad |= (off[i + 1] - off[i]) ^ d;

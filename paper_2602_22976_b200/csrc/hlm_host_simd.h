@@ -20,6 +20,11 @@ bool host_pack_weights_u8_scalar(const double* w, uint8_t* packed, uint64_t b, u
 bool host_offsets_differ(const uint64_t* off, uint64_t d, uint64_t b, uint64_t e);
 bool host_offsets_differ_scalar(const uint64_t* off, uint64_t d, uint64_t b, uint64_t e);
 
+// sizes[i] = off[i + 1] - off[i] for i in [b, e) as 16-bit values; true if some difference does not fit (or
+// the offsets decrease): the sizes are then meaningless.  Ragged instances ship these 2 bytes per edge instead
+// of 8 bytes of offset and the device rebuilds the offsets with a scan.
+bool host_pack_sizes_u16(const uint64_t* off, uint16_t* sizes, uint64_t b, uint64_t e);
+
 // which implementation the dispatcher picked: "avx2" or "scalar"
 const char* host_simd_level();
 

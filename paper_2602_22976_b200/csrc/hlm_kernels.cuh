@@ -1595,6 +1595,13 @@ __global__ void k_code_stats(const uint8_t* __restrict__ codes, uint32_t m, Weig
   }
 }
 
+// edge sizes as shipped by the host-assisted loader (16 bits each) -> the 32-bit input of the offset scan
+__global__ void k_widen_sizes(const uint16_t* __restrict__ s16, uint32_t* __restrict__ s32, uint64_t count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    s32[i] = s16[i];
+}
+
 __global__ void k_narrow_offsets(const uint64_t* off64, uint32_t* off32, uint64_t count) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)

@@ -27,7 +27,20 @@ def _variants(port):
     g4 = port.syn_generate(po.SYN_UNIFORM, n=20000, m=50000, d=4, seed=5, int_weights=False)
     out.append(("uniform d=4, unit weights: packed then folded to a constant", g4))
     g5 = port.syn_generate(po.SYN_NETLIST, n=30000, m=50000, seed=2, int_weights=True)
-    out.append(("ragged sizes: offsets raw, weights packed", g5))
+    out.append(("ragged sizes: 16-bit sizes instead of offsets, weights packed", g5))
+    g7 = port.generate_random(70000, 3, 2, 5, 9)
+    lists7 = [list(g7.edge_members[int(g7.edge_offsets[e]):int(g7.edge_offsets[e + 1])]) for e in range(g7.m)]
+    lists7.append(list(range(66000)))  # one edge of 66 000 pins: does not fit 16 bits, offsets raw
+    lists7 += [[e % 70000, (e * 7 + 1) % 70000 if (e * 7 + 1) % 70000 != e % 70000 else (e + 2) % 70000] for e in range(3000)]
+    out.append(("ragged with a 66 000-pin edge: offsets raw", po.graph_from_edge_lists(lists7, [1.0] * len(lists7), n=70000)))
+    g8 = port.generate_random(30000, 80000, 2, 2, 4)
+    lists8 = [list(g8.edge_members[int(g8.edge_offsets[e]):int(g8.edge_offsets[e + 1])]) for e in range(g8.m)]
+    for e in range(70000, 70050):  # uniform for the first 70 000 edges (beyond the loader's look-ahead), then ragged
+        v = 0
+        while v in lists8[e]:
+            v += 1
+        lists8[e].append(v)
+    out.append(("uniform prefix, ragged later: offsets raw", po.graph_from_edge_lists(lists8, [1.0] * g8.m, n=g8.n)))
     g6 = port.generate_random(30000, 50000, 3, 3, 4)
     lists = [list(g6.edge_members[int(g6.edge_offsets[e]):int(g6.edge_offsets[e + 1])]) for e in range(g6.m)]
     extra = 0
@@ -53,6 +66,10 @@ def test_one_shot_call_on_every_loader_path(hb, port, monkeypatch, assist):
             expect_bytes = g.edge_members.nbytes + g.edge_offsets.nbytes + g.base_weights.nbytes
             if assist and name.startswith("uniform d="):
                 assert got.report.h2d_bytes == g.edge_members.nbytes + g.m  # pins + one byte per weight
+            elif assist and "16-bit sizes" in name:
+                assert got.report.h2d_bytes == g.edge_members.nbytes + 2 * g.m + g.m  # pins + sizes + weight codes
+            elif assist and "offsets raw" in name and "last edge" not in name:
+                assert got.report.h2d_bytes >= g.edge_members.nbytes + g.edge_offsets.nbytes
             elif not assist:
                 assert got.report.h2d_bytes == expect_bytes
 
