@@ -263,6 +263,8 @@ struct BenchFlags {  // hlm_app.hpp:220-227
   std::vector<std::string> instances, variants = {"crcw"};
   std::vector<uint64_t> seeds = {1};
   uint32_t repeats = 3;
+  uint32_t warmup = 1;  // untimed runs per (instance, variant) first: CUDA context, module load, memory pools
+                        // (a B200 extension; the CPU reference has nothing to warm)
   RunFlags base;
   std::string csv_path;
 };
@@ -281,7 +283,18 @@ int cmd_bench(const BenchFlags& f) {  // hlm_app.hpp:232-333
     } catch (const std::exception& ex) {
       std::cerr << "error: " << path << ": " << ex.what() << "\n";
     }
-    for (const auto& variant : f.variants)
+    for (const auto& variant : f.variants) {
+      for (uint32_t w = 0; loaded && w < f.warmup; ++w) {
+        try {
+          RunFlags rf = f.base;
+          rf.instance.path = path;
+          rf.variant = variant;
+          rf.stream.seed = f.seeds.empty() ? 1 : f.seeds.front();
+          rf.emit_matching_path.clear();
+          (void)execute_run(rf, h);
+        } catch (const std::exception&) {  // reported by the timed runs below
+        }
+      }
       for (uint64_t seed : f.seeds)
         for (uint32_t rep = 0; rep < f.repeats; ++rep) {
           RunRow row;
@@ -309,6 +322,7 @@ int cmd_bench(const BenchFlags& f) {  // hlm_app.hpp:232-333
           }
           rows.push_back(std::move(row));
         }
+    }
   }
   std::map<std::pair<std::string, std::string>, std::vector<size_t>> by_pair;
   for (size_t i = 0; i < rows.size(); ++i)
@@ -512,7 +526,7 @@ const char* kUsage =
     "  run      --instance F [--format auto|hgr|metis] [--weights file|unit|random] [--weight-seed N] [--drop-isolated]\n"
     "           [--seed N] [--generator xorshift|park-miller|splitmix] [--noise LO:HI] [--uniform]\n"
     "           [--variant seq|crcw|crew|opt|greedy|auto] [--max-rounds N] [--csv F] [--emit-matching F] [--device N] [--gpus K]\n"
-    "  bench    --instances F... [--variants a,b] [--seeds 1,2] [--repeats N] [--csv F] + the instance / stream flags of run\n"
+    "  bench    --instances F... [--variants a,b] [--seeds 1,2] [--repeats N] [--warmup N] [--csv F] + the instance / stream flags of run\n"
     "  generate tight --d N --epsilon X --out F | random --n N --m M [--min-size A] [--max-size B] [--seed S]\n"
     "           [--weights unit|random] [--weight-seed S] --out F\n"
     "  verify   --instance F --matching F\n";
@@ -569,6 +583,8 @@ int run_cli(std::vector<std::string> argv) {
         for (const auto& s : split_commas(a.value(flag))) f.seeds.push_back(to_u64(s, flag));
       } else if (flag == "--repeats") {
         f.repeats = static_cast<uint32_t>(to_u64(a.value(flag), flag));
+      } else if (flag == "--warmup") {
+        f.warmup = static_cast<uint32_t>(to_u64(a.value(flag), flag));
       } else if (flag == "--workers") {
         f.base.workers = static_cast<unsigned>(to_u64(a.value(flag), flag));
       } else if (flag == "--max-rounds") {
