@@ -1229,12 +1229,15 @@ __global__ void k_advance(const RoundParams P, cudaGraphConditionalHandle handle
 }
 
 // ---------------------------------------------------------------------------------------------
-// All rounds of a small uniform instance in ONE cooperative launch.  When the whole instance sits
-// in L2 a round is a handful of dependent memory round trips, and three kernel launches per round
-// (sweep, check, advance: ~85 us per round inside the CUDA graph on config 1) cost several times
-// the work itself.  Here the resident grid runs sweep -> grid barrier -> check -> grid barrier ->
-// advance (one thread) -> grid barrier, round after round, until the status leaves ST_RUNNING (done,
-// round cap, tie, tag wrap: the host handles those exactly as after a graph launch).  The phases are
+// A whole matching of a small instance in ONE cooperative launch (which instances: fused_rounds_ok,
+// hlm_engine.cu).  When the instance sits in L2 a round is a handful of dependent memory round trips,
+// and three kernel launches per round (sweep, check, advance: ~85 us per round inside the CUDA graph
+// on config 1) plus the per-call memsets, read-backs and assembly kernels cost several times the work
+// itself.  Here the resident grid zeroes the per-call state, runs sweep -> grid barrier -> check (the
+// CTA that finishes it last advances the round) -> grid barrier, round after round, until the status
+// leaves ST_RUNNING (done, round cap; tie, tag wrap: the host handles those exactly as after a graph
+// launch and relaunches), then assembles the result into the caller's page-locked arrays.  D = 2, 4, 8:
+// uniform sizes; D = 0: any sizes (thread per edge, warp per edge above kLargeEdge pins).  The phases are
 // the bodies of the stand-alone kernels, so the results are the same by construction; the lists and
 // per-vertex words written in one phase are read in the next after the barrier's fence (the barrier of
 // cooperative groups ends with MEMBAR.GPU + CCTL.IVALL in every CTA, so ld.ca lines of the hot windows do
