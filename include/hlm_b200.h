@@ -121,7 +121,7 @@ typedef struct {
   double device_ms;                /* CUDA events around the round loop + result assembly */
   uint32_t tie_redo_rounds;        /* rounds that were redone on the exact three-level path */
   uint32_t kernel_launches;        /* kernels of this library launched by the call */
-  uint32_t graph_launches;         /* CUDA-graph launches (each runs many rounds) */
+  uint32_t graph_launches;         /* CUDA-graph launches, or launches of the one-kernel form of small instances (each runs many rounds) */
   uint32_t write_conflicts;        /* always 0 (RunReport::write_conflicts) */
   /* HLM_B200_FLAG_KERNEL_TIMES: rounds + 1 entries each (the last filter launch finds the empty
    * list); NULL otherwise.  CRCW engine: filter = the round sweep (invalidate + compact + vertex-max, all
