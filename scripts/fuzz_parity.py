@@ -119,6 +119,11 @@ while time.time() < t_end and not bad:
         sh.release()
     if it % 4 == 0:
         check("host arrays, num_gpus", hb.run_variant(hg, hs, hb.ParallelConfig(num_gpus=int(rng.integers(2, 6)))), want, what)
+    if it % 5 == 0:
+        # the host-assisted loader on small instances (threshold lowered): uniformity scan, weight codes, 16-bit sizes
+        os.environ["HLM_B200_ASSIST_MIN_EDGES"] = "2"
+        check("host arrays, assisted loader", hb.run_variant(hg, hs, hb.ParallelConfig(variant="auto")), want, what)
+        os.environ.pop("HLM_B200_ASSIST_MIN_EDGES", None)
 print(f"{it} instances in {budget:.0f} s")
 for k, v in sorted(counts.items()):
     print(f"  {k:28s} {v} matchings compared with the oracle: {'ok' if not any(b[0] == k for b in bad) else 'MISMATCH'}")

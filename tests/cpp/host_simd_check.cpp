@@ -72,6 +72,34 @@ int main() {
       }
     }
   }
+  // 16-bit edge sizes of ragged instances: exact where every size fits, flagged otherwise
+  {
+    std::mt19937_64 r2(7);
+    for (size_t n : {1u, 3u, 64u, 1000u, 70001u}) {
+      std::vector<uint64_t> off(n + 1, 0);
+      for (size_t i = 0; i < n; ++i) off[i + 1] = off[i] + r2() % 70;  // sizes 0..69
+      std::vector<uint16_t> sz(n, 0xABCD);
+      check(!host_pack_sizes_u16(off.data(), sz.data(), 0, n), "sizes fit");
+      bool same = true;
+      for (size_t i = 0; i < n; ++i) same &= sz[i] == off[i + 1] - off[i];
+      check(same, "sizes exact");
+      if (n >= 3) {  // a sub-range leaves the rest alone
+        std::vector<uint16_t> part(n, 0xABCD);
+        check(!host_pack_sizes_u16(off.data(), part.data(), 1, n - 1), "sub-range fits");
+        check(part[0] == 0xABCD && part[n - 1] == 0xABCD && part[1] == off[2] - off[1], "sub-range only");
+      }
+      std::vector<uint64_t> big(off);
+      for (size_t i = n / 2 + 1; i <= n; ++i) big[i] += 65536;  // one edge of >= 65 536 pins
+      check(host_pack_sizes_u16(big.data(), sz.data(), 0, n), "size beyond 16 bits");
+      big[n / 2 + 1] = 65535 + big[n / 2];
+      if (n >= 2) {
+        std::vector<uint64_t> dec(off);
+        dec[n / 2 + 1] = dec[n / 2] + 5;
+        dec[n / 2] += 9;  // offsets decrease across one edge
+        if (dec[n / 2 + 1] < dec[n / 2]) check(host_pack_sizes_u16(dec.data(), sz.data(), 0, n), "decreasing offsets");
+      }
+    }
+  }
   std::printf("host simd (%s): %s\n", host_simd_level(), fails ? "FAILED" : "ok");
   return fails ? 1 : 0;
 }
